@@ -1,0 +1,102 @@
+/*
+ * wl_dwt.h -- C-ABI of the B200-native 2-D lifting DWT (libwavelift_b200.so).
+ *
+ * Drop-in boundary for the reference's transform API
+ * (/root/reference/proj/include/wavelift/transform.hpp). Every entry point
+ * takes plain pointers and sizes; image and subband buffers are caller-owned
+ * DEVICE memory (float32, row-major, pitches in ELEMENTS) and work is
+ * enqueued on the caller's CUDA stream (NULL = legacy default stream).
+ * Host-buffer (float64 Image/QuadGrid/Pyramid) parity wrappers live in the
+ * C++ header wavelift_b200.hpp on top of this ABI.
+ *
+ * Enumerations follow the reference:
+ *   wavelet  : WL_CDF53, WL_CDF97, WL_DD137            (wavelets.cpp:27-62)
+ *   scheme   : SchemeKind order                        (schemes.hpp:15-26)
+ *   boundary : WL_PERIODIC, WL_SYMMETRIC               (transform.hpp:44)
+ * Status codes mirror the reference's exception classes
+ * (wavelift_main.cpp:363-369): WL_OK, WL_EINVAL (std::invalid_argument),
+ * WL_ERUNTIME (CUDA / other runtime failure). wl_last_error() returns the
+ * message of the calling thread's last failure.
+ */
+#ifndef WL_DWT_H_
+#define WL_DWT_H_
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { WL_OK = 0, WL_EINVAL = 1, WL_ERUNTIME = 2 };
+enum { WL_CDF53 = 0, WL_CDF97 = 1, WL_DD137 = 2 };
+enum {
+    WL_SWELDENS = 0, WL_IWAHASHI, WL_IWAHASHI_STAR, WL_EXPLOSIVE, WL_EXPLOSIVE_STAR,
+    WL_MONOLITHIC, WL_MONOLITHIC_STAR, WL_POLYPHASE, WL_POLYPHASE_STAR, WL_CONVOLUTION
+};
+enum { WL_PERIODIC = 0, WL_SYMMETRIC = 1 };
+enum { WL_FORWARD = 0, WL_INVERSE = 1 };
+
+/* Message of this thread's last non-OK status (empty string if none). */
+const char* wl_last_error(void);
+/* Library version / build string. */
+const char* wl_version(void);
+
+/* Cost and structure of a (wavelet, scheme, direction) program:
+ * barriers = count_barriers (schemes.cpp:193-198), macs = count_macs
+ * (schemes.cpp:176-191), epochs = block barriers per tile in the kernel,
+ * halo = tile halo in component cells (parsim.cpp:185-218 required_halo).
+ * Replaces schemes.hpp:58-62. */
+int wl_scheme_info(int wavelet, int scheme, int direction, int* barriers, long* macs,
+                   int* epochs, int* halo);
+
+/* transform.cpp:59-72 resolve_index (host-side helper). */
+int wl_resolve_index(int i, int n, int boundary);
+
+/* One level, forward: replaces `QuadGrid forward(const Image&, const Scheme&,
+ * BoundaryMode, bool apply_scaling)` (transform.hpp:65-66, transform.cpp:163-176).
+ * img: w x h (even, positive), img_pitch >= w. Output planes LL, HL, LH, HH are
+ * (w/2) x (h/2) with plane_pitch >= w/2. */
+int wl_dwt2_forward(const float* img, int w, int h, long img_pitch, int wavelet, int scheme,
+                    int boundary, int scaling, float* ll, float* hl, float* lh, float* hh,
+                    long plane_pitch, void* stream);
+
+/* One level, inverse: replaces `Image inverse(const QuadGrid&, const
+ * WaveletSpec&, BoundaryMode, bool undo_scaling)` (transform.hpp:71-72,
+ * transform.cpp:178-196). `scheme` selects the inverse kernel: WL_SWELDENS is
+ * the reference's own algorithm (reversed negated separable steps); every
+ * other lifting scheme runs its own reversed, inverted step list with the
+ * same barrier count as its forward (identical result under the periodic
+ * boundary; see DESIGN.md for the symmetric-boundary semantics).
+ * WL_CONVOLUTION maps to WL_SWELDENS. */
+int wl_dwt2_inverse(const float* ll, const float* hl, const float* lh, const float* hh, int qw,
+                    int qh, long plane_pitch, int wavelet, int scheme, int boundary,
+                    int undo_scaling, float* img, long img_pitch, void* stream);
+
+/* Multi-level pyramid, replaces multi_level_forward / multi_level_inverse
+ * (transform.hpp:87-91, transform.cpp:198-256). Flat pyramid layout (device,
+ * densely packed): for each level l = 0..levels-1 (finest first) the HL, LH, HH
+ * planes of (w>>(l+1)) x (h>>(l+1)), then the coarsest LL plane -- the
+ * subband_io payload order (subband_io.hpp:7-20). `scratch` must hold
+ * wl_pyramid_scratch_elems(w, h, levels) floats. */
+size_t wl_pyramid_elems(int w, int h, int levels);
+size_t wl_pyramid_scratch_elems(int w, int h, int levels);
+int wl_dwt2_pyramid_forward(const float* img, int w, int h, int levels, int wavelet, int scheme,
+                            int boundary, int scaling, float* pyramid, float* scratch,
+                            void* stream);
+int wl_dwt2_pyramid_inverse(const float* pyramid, int w, int h, int levels, int wavelet,
+                            int scheme, int boundary, int undo_scaling, float* img,
+                            float* scratch, void* stream);
+
+/* Engine selection for tests/benchmarks: 0 = auto (fast register-tile engine
+ * where available, generic tile interpreter otherwise), 1 = force the generic
+ * interpreter, 2 = force the fast engine (WL_EINVAL where unsupported).
+ * Returns the previous value. Process-global. */
+int wl_set_engine(int engine);
+/* Number of kernel launches this library issued so far (process-global). */
+long wl_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* WL_DWT_H_ */

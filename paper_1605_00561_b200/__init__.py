@@ -1,0 +1,282 @@
+"""wavelift_b200 -- B200-native 2-D lifting DWT (CDF 5/3, CDF 9/7; all schemes).
+
+Python host side of the drop-in surface. It mirrors the reference's C++
+transform API (``/root/reference/proj/include/wavelift/transform.hpp:14-95``,
+``schemes.hpp:15-62``, ``wavelets.hpp:21-32``) over device ``torch`` tensors and
+calls the CUDA kernels through the C-ABI in ``include/wl_dwt.h``
+(``libwavelift_b200.so``, built in-tree for sm_100a). There is no CPU
+fallback: without the library or a GPU every call raises.
+
+Names follow the reference: ``get_wavelet``, ``build_scheme``,
+``parse_scheme`` / ``scheme_name``, ``parse_boundary`` / ``boundary_name``,
+``forward``, ``inverse``, ``multi_level_forward``, ``multi_level_inverse``,
+``resolve_index``. Errors map to the reference's exception classes:
+``ValueError`` for ``std::invalid_argument`` and ``RuntimeError`` otherwise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+from .schemes import BOUNDARIES, SCHEMES, WAVELETS  # noqa: F401
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libwavelift_b200.so")
+
+WL_OK, WL_EINVAL, WL_ERUNTIME = 0, 1, 2
+ENGINE_AUTO, ENGINE_INTERP, ENGINE_FAST = 0, 1, 2
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Loads libwavelift_b200.so (raises if it was not built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} missing -- run __graft_entry__.build() "
+                               "(no CPU fallback exists)")
+        l = ctypes.CDLL(LIB_PATH)
+        vp, i, lg, fp = ctypes.c_void_p, ctypes.c_int, ctypes.c_long, ctypes.c_void_p
+        l.wl_last_error.restype = ctypes.c_char_p
+        l.wl_version.restype = ctypes.c_char_p
+        l.wl_scheme_info.argtypes = [i, i, i, ctypes.POINTER(i), ctypes.POINTER(lg),
+                                     ctypes.POINTER(i), ctypes.POINTER(i)]
+        l.wl_resolve_index.argtypes = [i, i, i]
+        l.wl_dwt2_forward.argtypes = [fp, i, i, lg, i, i, i, i, fp, fp, fp, fp, lg, vp]
+        l.wl_dwt2_inverse.argtypes = [fp, fp, fp, fp, i, i, lg, i, i, i, i, fp, lg, vp]
+        l.wl_pyramid_elems.restype = ctypes.c_size_t
+        l.wl_pyramid_elems.argtypes = [i, i, i]
+        l.wl_pyramid_scratch_elems.restype = ctypes.c_size_t
+        l.wl_pyramid_scratch_elems.argtypes = [i, i, i]
+        l.wl_dwt2_pyramid_forward.argtypes = [fp, i, i, i, i, i, i, i, fp, fp, vp]
+        l.wl_dwt2_pyramid_inverse.argtypes = [fp, i, i, i, i, i, i, i, fp, fp, vp]
+        l.wl_set_engine.argtypes = [i]
+        l.wl_launch_count.restype = lg
+        _lib = l
+    return _lib
+
+
+def _check(status: int):
+    if status == WL_OK:
+        return
+    msg = lib().wl_last_error().decode()
+    if status == WL_EINVAL:
+        raise ValueError(msg)
+    raise RuntimeError(msg)
+
+
+def version() -> str:
+    return lib().wl_version().decode()
+
+
+def set_engine(engine: int) -> int:
+    """0 auto, 1 generic tile interpreter, 2 fast register-tile engine."""
+    return lib().wl_set_engine(engine)
+
+
+def launch_count() -> int:
+    return lib().wl_launch_count()
+
+
+# ---------------------------------------------------------------- selection
+def _index(table, name, what):
+    if isinstance(name, int):
+        if 0 <= name < len(table):
+            return name
+    elif name in table:
+        return table.index(name)
+    raise ValueError(f"unknown {what}: {name}")
+
+
+def scheme_name(kind) -> str:
+    """schemes.cpp:17-31."""
+    return SCHEMES[_index(SCHEMES, kind, "scheme")]
+
+
+def parse_scheme(name: str):
+    """schemes.cpp:33-37: None for unknown names."""
+    return SCHEMES.index(name) if name in SCHEMES else None
+
+
+def boundary_name(mode) -> str:
+    return BOUNDARIES[_index(BOUNDARIES, mode, "boundary")]
+
+
+def parse_boundary(name: str):
+    return BOUNDARIES.index(name) if name in BOUNDARIES else None
+
+
+@dataclass(frozen=True)
+class WaveletSpec:
+    """wavelets.hpp:21-27 (constants live in the kernels' generated tables)."""
+    name: str
+    index: int
+    zeta: float
+
+
+def get_wavelet(name: str) -> WaveletSpec:
+    """wavelets.cpp:27-62; ValueError for unknown names."""
+    from .schemes import get_wavelet as _gw
+    w = _gw(name)
+    return WaveletSpec(w.name, WAVELETS.index(w.name), w.zeta)
+
+
+@dataclass(frozen=True)
+class Scheme:
+    """schemes.hpp:40-45, reduced to the selection the kernels need."""
+    kind: int
+    wavelet: WaveletSpec
+
+    @property
+    def name(self) -> str:
+        return SCHEMES[self.kind]
+
+    def info(self, direction: int = 0) -> dict:
+        b, m, e, h = ctypes.c_int(), ctypes.c_long(), ctypes.c_int(), ctypes.c_int()
+        _check(lib().wl_scheme_info(self.wavelet.index, self.kind, direction, ctypes.byref(b),
+                                    ctypes.byref(m), ctypes.byref(e), ctypes.byref(h)))
+        return {"barriers": b.value, "macs": m.value, "epochs": e.value, "halo": h.value}
+
+
+def build_scheme(kind, wavelet) -> Scheme:
+    """schemes.cpp:146-174 (selection only)."""
+    w = wavelet if isinstance(wavelet, WaveletSpec) else get_wavelet(wavelet)
+    return Scheme(_index(SCHEMES, kind, "scheme"), w)
+
+
+def count_barriers(s: Scheme) -> int:
+    return s.info()["barriers"]
+
+
+def count_macs(s: Scheme) -> int:
+    return s.info()["macs"]
+
+
+def resolve_index(i: int, n: int, boundary) -> int:
+    return lib().wl_resolve_index(i, n, _index(BOUNDARIES, boundary, "boundary"))
+
+
+# ----------------------------------------------------------------- transforms
+def _stream_ptr(stream):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _dev_f32(t, what):
+    import torch
+    if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != torch.float32:
+        raise ValueError(f"{what} must be a float32 CUDA tensor")
+    return t
+
+
+def _pitched(t):
+    """(ptr, rows, cols, pitch) for a 2-D tensor with unit column stride."""
+    if t.dim() != 2 or t.stride(1) != 1:
+        t = t.contiguous()
+    return t, t.stride(0)
+
+
+def forward(img, scheme: Scheme, boundary="periodic", apply_scaling=False, out=None,
+            stream=None):
+    """transform.cpp:163-176: (h, w) float32 CUDA image -> (4, h/2, w/2) planes
+    [LL, HL, LH, HH]."""
+    import torch
+    img = _dev_f32(img, "img")
+    if img.dim() != 2:
+        raise ValueError("img must be 2-D (height, width)")
+    img, pitch = _pitched(img)
+    h, w = img.shape
+    if out is None:
+        out = torch.empty((4, max(h // 2, 0), max(w // 2, 0)), device=img.device,
+                          dtype=torch.float32)
+    b = _index(BOUNDARIES, boundary, "boundary")
+    p = [out[c].data_ptr() for c in range(4)]
+    _check(lib().wl_dwt2_forward(img.data_ptr(), w, h, pitch, scheme.wavelet.index, scheme.kind,
+                                 b, int(bool(apply_scaling)), p[0], p[1], p[2], p[3],
+                                 out.stride(1) if out.dim() == 3 else w // 2,
+                                 _stream_ptr(stream)))
+    return out
+
+
+def inverse(q, wavelet, boundary="periodic", undo_scaling=False, scheme=None, out=None,
+            stream=None):
+    """transform.cpp:178-196. `q` is (4, qh, qw). `scheme` picks the inverse
+    kernel (default: the reference's separable/Sweldens inverse)."""
+    import torch
+    q = _dev_f32(q, "q").contiguous()
+    if q.dim() != 3 or q.shape[0] != 4:
+        raise ValueError("q must be (4, qh, qw)")
+    w = wavelet if isinstance(wavelet, WaveletSpec) else get_wavelet(wavelet)
+    kind = 0 if scheme is None else (scheme.kind if isinstance(scheme, Scheme)
+                                     else _index(SCHEMES, scheme, "scheme"))
+    _, qh, qw = q.shape
+    if out is None:
+        out = torch.empty((2 * qh, 2 * qw), device=q.device, dtype=torch.float32)
+    b = _index(BOUNDARIES, boundary, "boundary")
+    _check(lib().wl_dwt2_inverse(q[0].data_ptr(), q[1].data_ptr(), q[2].data_ptr(),
+                                 q[3].data_ptr(), qw, qh, qw, w.index, kind, b,
+                                 int(bool(undo_scaling)), out.data_ptr(), out.stride(0),
+                                 _stream_ptr(stream)))
+    return out
+
+
+@dataclass
+class Pyramid:
+    """transform.hpp:74-83 over one flat device buffer: details finest first
+    (hl, lh, hh views per level) and the coarsest ll view."""
+    flat: object
+    width: int
+    height: int
+    levels: int
+
+    def level(self, l):
+        w, h = self.width >> (l + 1), self.height >> (l + 1)
+        off = sum(3 * (self.width >> (k + 1)) * (self.height >> (k + 1)) for k in range(l))
+        n = w * h
+        return tuple(self.flat[off + i * n: off + (i + 1) * n].view(h, w) for i in range(3))
+
+    @property
+    def ll(self):
+        w, h = self.width >> self.levels, self.height >> self.levels
+        return self.flat[self.flat.numel() - w * h:].view(h, w)
+
+
+def multi_level_forward(img, scheme: Scheme, levels: int, boundary="periodic",
+                        apply_scaling=False, stream=None) -> Pyramid:
+    """transform.cpp:198-227."""
+    import torch
+    img = _dev_f32(img, "img").contiguous()
+    h, w = img.shape
+    n = lib().wl_pyramid_elems(w, h, levels)
+    flat = torch.empty(max(n, 1), device=img.device, dtype=torch.float32)
+    scratch = torch.empty(max(lib().wl_pyramid_scratch_elems(w, h, levels), 1),
+                          device=img.device, dtype=torch.float32)
+    _check(lib().wl_dwt2_pyramid_forward(img.data_ptr(), w, h, levels, scheme.wavelet.index,
+                                         scheme.kind, _index(BOUNDARIES, boundary, "boundary"),
+                                         int(bool(apply_scaling)), flat.data_ptr(),
+                                         scratch.data_ptr(), _stream_ptr(stream)))
+    return Pyramid(flat, w, h, levels)
+
+
+def multi_level_inverse(pyr: Pyramid, wavelet, boundary="periodic", undo_scaling=False,
+                        scheme=None, stream=None):
+    """transform.cpp:229-256."""
+    import torch
+    w = wavelet if isinstance(wavelet, WaveletSpec) else get_wavelet(wavelet)
+    kind = 0 if scheme is None else (scheme.kind if isinstance(scheme, Scheme)
+                                     else _index(SCHEMES, scheme, "scheme"))
+    flat = _dev_f32(pyr.flat, "pyramid").contiguous()
+    if flat.numel() != pyr.width * pyr.height:
+        raise ValueError("pyramid detail plane size does not match its level")
+    out = torch.empty((pyr.height, pyr.width), device=flat.device, dtype=torch.float32)
+    scratch = torch.empty(max(lib().wl_pyramid_scratch_elems(pyr.width, pyr.height,
+                                                              pyr.levels), 1),
+                          device=flat.device, dtype=torch.float32)
+    _check(lib().wl_dwt2_pyramid_inverse(flat.data_ptr(), pyr.width, pyr.height, pyr.levels,
+                                         w.index, kind, _index(BOUNDARIES, boundary, "boundary"),
+                                         int(bool(undo_scaling)), out.data_ptr(),
+                                         scratch.data_ptr(), _stream_ptr(stream)))
+    return out

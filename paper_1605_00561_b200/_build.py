@@ -1,0 +1,93 @@
+"""In-tree build of libwavelift_b200.so (sm_100a) and the CPU oracle.
+
+`python -m paper_1605_00561_b200._build` or `__graft_entry__.build()`.
+nvcc cross-compiles for sm_100a without a GPU; the .so lands next to this
+file so it travels to the GPU box with the repo snapshot.
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+from concurrent.futures import ThreadPoolExecutor
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+OBJ = os.path.join(PKG, "_obj")
+LIB = os.path.join(PKG, "libwavelift_b200.so")
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
+                "--expt-relaxed-constexpr", "-Xptxas", "-v", "-ccbin", "g++",
+                "-I" + os.path.join(ROOT, "include")]
+SOURCES = ["wl_capi.cu", "wl_interp.cu", "wl_fast.cu"]
+
+
+def _deps():
+    files = []
+    for d in (CSRC, os.path.join(CSRC, "gen"), os.path.join(ROOT, "include")):
+        if os.path.isdir(d):
+            files += [os.path.join(d, f) for f in os.listdir(d)
+                      if f.endswith((".h", ".cuh", ".hpp"))]
+    return files
+
+
+def _newer(target, sources):
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(s) > t for s in sources)
+
+
+def _compile(src, verbose):
+    obj = os.path.join(OBJ, os.path.basename(src).replace(".cu", ".o"))
+    if not _newer(obj, [src, *_deps(), __file__]):
+        return obj, ""
+    cmd = [NVCC, *FLAGS, "-c", src, "-o", obj]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")
+    log = r.stdout + r.stderr
+    with open(obj + ".ptxas.txt", "w") as f:
+        f.write(log)
+    return obj, log if verbose else ""
+
+
+def gen_tables():
+    subprocess.run([sys.executable, os.path.join(ROOT, "tools", "gen_steps.py")], check=True,
+                   capture_output=True)
+
+
+def build_lib(verbose=False) -> str:
+    gen_tables()
+    os.makedirs(OBJ, exist_ok=True)
+    srcs = [os.path.join(CSRC, s) for s in SOURCES]
+    with ThreadPoolExecutor(max_workers=len(srcs)) as ex:
+        res = list(ex.map(lambda s: _compile(s, verbose), srcs))
+    objs = [o for o, _ in res]
+    for _, log in res:
+        if log:
+            print(log)
+    if _newer(LIB, objs):
+        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-ccbin", "g++"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
+    return LIB
+
+
+def build_oracle():
+    r = subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle")], capture_output=True,
+                       text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"oracle build failed:\n{r.stdout}\n{r.stderr}")
+
+
+def build(verbose=False):
+    build_oracle()
+    return build_lib(verbose)
+
+
+if __name__ == "__main__":
+    print(build(verbose="-v" in sys.argv))

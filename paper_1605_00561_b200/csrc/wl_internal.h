@@ -1,0 +1,33 @@
+// Internal declarations shared by the kernels and the C-ABI layer.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "wl_program.h"
+
+// One single-level transform launch (forward: image -> 4 planes; inverse:
+// 4 planes -> image). Pitches are in elements.
+struct WlLevel {
+    const float* in[4];  // fwd: in[0] = image; inv: LL, HL, LH, HH
+    float* out[4];       // fwd: LL, HL, LH, HH; inv: out[0] = image
+    int qw, qh;          // component-grid (plane) size; image is 2qw x 2qh
+    long in_pitch, out_pitch;
+    int prog;            // program index ((wavelet*10)+scheme)*2+direction
+    int wavelet, scheme, direction;
+    int boundary;        // 0 periodic, 1 symmetric
+    int scaling;         // apply (fwd) / undo (inv) the zeta^2 scaling step
+};
+
+const WlProgram& wl_host_program(int prog);
+const WlStep* wl_host_steps();
+
+// Generic tile interpreter: every wavelet/scheme/direction/boundary.
+cudaError_t wl_launch_interp(const WlLevel& L, cudaStream_t stream);
+// Direct 2-D convolution forward (SchemeKind::Convolution).
+cudaError_t wl_launch_conv(const WlLevel& L, cudaStream_t stream);
+// Fast register-tile engine; returns cudaErrorNotSupported when the
+// (wavelet, scheme, direction) has no fast instantiation.
+cudaError_t wl_launch_fast(const WlLevel& L, cudaStream_t stream);
+bool wl_fast_supported(const WlLevel& L);
+
+void wl_count_launch();
