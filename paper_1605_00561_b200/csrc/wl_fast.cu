@@ -1,6 +1,110 @@
-// Fast register-tile engine (placeholder until the tuned kernels land).
-#include "wl_internal.h"
+// Fast register-tile engine: host side (TMA descriptors, tile plan, frame
+// hand-off to the interpreter, dispatch to the per-(wavelet, direction)
+// instantiation units wl_fast_<wavelet>_<dir>.cu).
+#include <cstdint>
 
-bool wl_fast_supported(const WlLevel&) { return false; }
+#include "wl_fast_impl.cuh"
 
-cudaError_t wl_launch_fast(const WlLevel&, cudaStream_t) { return cudaErrorNotSupported; }
+namespace wlfast {
+
+EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) !=
+                cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return static_cast<EncodeTiledFn>(nullptr);
+        return reinterpret_cast<EncodeTiledFn>(p);
+    }();
+    return fn;
+}
+
+bool make_map(CUtensorMap* m, const float* base, int w, int h, long pitch, int box_w,
+              int box_h) {
+    EncodeTiledFn enc = encode_fn();
+    if (!enc) return false;
+    if ((reinterpret_cast<uintptr_t>(base) & 15) || ((pitch * 4) & 15)) return false;
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(w), static_cast<cuuint64_t>(h)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(pitch) * 4};
+    const cuuint32_t box[2] = {static_cast<cuuint32_t>(box_w), static_cast<cuuint32_t>(box_h)};
+    const cuuint32_t es[2] = {1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides,
+               box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace wlfast
+
+cudaError_t wl_fast_cdf53_fwd(int scheme, const WlLevel& L, const wlfast::Plan& p,
+                              cudaStream_t s);
+cudaError_t wl_fast_cdf53_inv(int scheme, const WlLevel& L, const wlfast::Plan& p,
+                              cudaStream_t s);
+cudaError_t wl_fast_cdf97_fwd(int scheme, const WlLevel& L, const wlfast::Plan& p,
+                              cudaStream_t s);
+cudaError_t wl_fast_cdf97_inv(int scheme, const WlLevel& L, const wlfast::Plan& p,
+                              cudaStream_t s);
+
+namespace {
+
+void geometry(const WlLevel& L, int* R, int* NW) {
+    if (L.wavelet == 0) {
+        *R = wlfast::Config<0>::R;
+        *NW = wlfast::Config<0>::NW;
+    } else {
+        *R = wlfast::Config<1>::R;
+        *NW = wlfast::Config<1>::NW;
+    }
+}
+
+bool aligned(const void* p, int bytes) { return (reinterpret_cast<uintptr_t>(p) % bytes) == 0; }
+
+}  // namespace
+
+bool wl_fast_supported(const WlLevel& L) {
+    if (L.wavelet < 0 || L.wavelet > 1 || L.scheme < 0 || L.scheme > 8) return false;
+    if (!wlfast::encode_fn()) return false;
+    if (L.direction == 0) {
+        if (!aligned(L.in[0], 16) || (L.in_pitch % 4) != 0) return false;
+        for (int k = 0; k < 4; ++k)
+            if (!aligned(L.out[k], 8)) return false;
+        if (L.out_pitch % 2 != 0) return false;
+    } else {
+        for (int k = 0; k < 4; ++k)
+            if (!aligned(L.in[k], 16)) return false;
+        if ((L.in_pitch % 4) != 0 || !aligned(L.out[0], 16) || (L.out_pitch % 4) != 0)
+            return false;
+    }
+    int R, NW;
+    geometry(L, &R, &NW);
+    const int H = wl_host_program(L.prog).halo;
+    return wlfast::plan_tiles(L, H, R, NW).ok;
+}
+
+cudaError_t wl_launch_fast(const WlLevel& L, cudaStream_t stream) {
+    if (!wl_fast_supported(L)) return cudaErrorNotSupported;
+    int R, NW;
+    geometry(L, &R, &NW);
+    const int H = wl_host_program(L.prog).halo;
+    const wlfast::Plan plan = wlfast::plan_tiles(L, H, R, NW);
+    cudaError_t e;
+    if (L.wavelet == 0)
+        e = L.direction == 0 ? wl_fast_cdf53_fwd(L.scheme, L, plan, stream)
+                             : wl_fast_cdf53_inv(L.scheme, L, plan, stream);
+    else
+        e = L.direction == 0 ? wl_fast_cdf97_fwd(L.scheme, L, plan, stream)
+                             : wl_fast_cdf97_inv(L.scheme, L, plan, stream);
+    if (e != cudaSuccess) return e;
+    // The frame around the tile grid (image borders included) goes to the
+    // interpreter, which resolves boundaries exactly per step.
+    const int Y0 = plan.args.Y0, X0 = plan.args.X0;
+    const int Y1 = Y0 + plan.tiles_y * plan.args.TH, X1 = X0 + plan.args.tiles_x * plan.args.TW;
+    WlRects fr{};
+    fr.n = 4;
+    fr.y0[0] = 0;  fr.x0[0] = 0;  fr.ny[0] = Y0;          fr.nx[0] = L.qw;       // top
+    fr.y0[1] = Y1; fr.x0[1] = 0;  fr.ny[1] = L.qh - Y1;   fr.nx[1] = L.qw;       // bottom
+    fr.y0[2] = Y0; fr.x0[2] = 0;  fr.ny[2] = Y1 - Y0;     fr.nx[2] = X0;         // left
+    fr.y0[3] = Y0; fr.x0[3] = X1; fr.ny[3] = Y1 - Y0;     fr.nx[3] = L.qw - X1;  // right
+    return wl_launch_interp_rects(L, fr, stream);
+}

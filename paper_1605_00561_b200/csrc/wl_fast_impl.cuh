@@ -1,0 +1,467 @@
+// Fast register-tile engine for the cdf53 / cdf97 lifting schemes.
+//
+// Persistent CTAs; warp-specialised:
+//   * 1 producer warp streams tiles HBM -> shared memory with TMA
+//     (cp.async.bulk.tensor.2d) into a 2-stage ring guarded by mbarriers
+//     ("full": transaction-count barrier armed with the stage's bytes;
+//     "empty": one arrival per compute warp once it has copied its rows).
+//   * NW compute warps hold the tile in registers: warp w owns R rows of
+//     component cells, lane l owns CPT=2 adjacent cells of each row, i.e. a
+//     64-cell-wide x (NW*R)-cell-tall compute region per tile. The 2x2 pixel
+//     de-interleave of polyphase_split (transform.cpp:74-86) happens in the
+//     LDS.128 of two pixel rows.
+//   * Every lifting step runs on registers. Horizontal neighbours come from
+//     the adjacent lane by warp shuffle; vertical neighbours from the same
+//     lane's registers, except at the warp's top/bottom row, where they come
+//     from the neighbouring warp through shared memory. That exchange is the
+//     ONLY cross-warp dependency, so each tile executes exactly one
+//     bar.sync per epoch after the first (whose neighbour rows are read
+//     straight from the TMA stage, behind the mbarrier wait): block
+//     barriers per tile == count_barriers of the scheme (schemes.cpp:193-198).
+//   * Redundant halo: the outer H cells of the compute region (H = the
+//     program's reach, = parsim required_halo) are computed but not stored;
+//     output tile = (64 - 2H) x (NW*R - 2H) cells.
+//
+// Only tiles whose compute region (plus one ghost row above and below) lies
+// inside the image are processed here; they are identical for the periodic
+// and symmetric boundaries. The thin frame outside the tile grid is handled
+// by the generic interpreter (wl_interp.cu), which implements the per-step
+// boundary resolution of transform.cpp:114-115 exactly.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdlib>
+#include <utility>
+
+#include "gen/fast_gen.cuh"
+#include "wl_internal.h"
+
+namespace wlfast {
+
+constexpr int CPT = 2;   // component cells per lane per row
+constexpr int TWC = 64;  // compute-region width in cells (32 lanes x CPT)
+
+template <class F, int... I>
+__device__ __forceinline__ void sfor_impl(F&& f, std::integer_sequence<int, I...>) {
+    (f(std::integral_constant<int, I>{}), ...);
+}
+template <int N, class F>
+__device__ __forceinline__ void sfor(F&& f) {
+    sfor_impl(f, std::make_integer_sequence<int, N>{});
+}
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WL_WAIT:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WL_WAIT;\n}" ::"r"(smem_u32(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int x, int y) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void named_sync(int id, int nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+struct FastArgs {
+    float* out[4];   // fwd: LL, HL, LH, HH planes; inv: out[0] = image
+    long out_pitch;  // elements
+    int tiles_x, ntiles;
+    int X0, Y0;      // first output cell of tile (0, 0)
+    int TW, TH;      // output tile size in cells
+    int scaling;
+    float scale;
+};
+
+template <int R, int NW>
+struct Geometry {
+    static constexpr int kRows = NW * R + 2;                 // cell rows per stage incl. ghosts
+    static constexpr int kStageFloats = 4 * TWC * kRows;     // == 2*TWC px * 2*kRows px
+    static constexpr int kStageBytes = kStageFloats * 4;
+    static constexpr int kXchFloats = 2 * NW * 2 * 32 * CPT * 4;
+    static constexpr size_t kSmemBytes =
+        2 * (size_t)kStageBytes + (size_t)kXchFloats * 4 + 64;
+};
+
+// Neighbour accessor for the cell at (row RR, column CC) of the lane's block.
+template <int R, int RR, int CC>
+struct Acc {
+    const float (&v)[R][CPT][4];
+    const float (&gu)[CPT][4];
+    const float (&gd)[CPT][4];
+    const float (&sl)[R + 2][4];
+    const float (&sr)[R + 2][4];
+    template <int C, int DR, int DC>
+    __device__ __forceinline__ float g() const {
+        constexpr int r = RR + DR, c = CC + DC;
+        if constexpr (c < 0)
+            return sl[r + 1][C];
+        else if constexpr (c >= CPT)
+            return sr[r + 1][C];
+        else if constexpr (r < 0)
+            return gu[c][C];
+        else if constexpr (r >= R)
+            return gd[c][C];
+        else
+            return v[r][c][C];
+    }
+};
+
+// kUse bit layout (gen_steps.py usage_mask): comp*9 + (dr+1)*3 + (dc+1).
+__host__ __device__ constexpr bool uses(unsigned long long m, int c, int dr, int dc) {
+    return (m >> (c * 9 + (dr + 1) * 3 + (dc + 1))) & 1ull;
+}
+__host__ __device__ constexpr bool uses_dc(unsigned long long m, int c, int dc) {
+    return uses(m, c, -1, dc) || uses(m, c, 0, dc) || uses(m, c, 1, dc);
+}
+__host__ __device__ constexpr bool uses_dr(unsigned long long m, int c, int dr) {
+    return uses(m, c, dr, -1) || uses(m, c, dr, 0) || uses(m, c, dr, 1);
+}
+
+template <class P, int DIR, int R, int NW>
+__global__ void __launch_bounds__((NW + 1) * 32)
+    fast_kernel(const __grid_constant__ CUtensorMap m0, const __grid_constant__ CUtensorMap m1,
+                const __grid_constant__ CUtensorMap m2, const __grid_constant__ CUtensorMap m3,
+                const FastArgs a) {
+    using G = Geometry<R, NW>;
+    constexpr int H = P::kHalo;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    float* stage = reinterpret_cast<float*>(smem_raw);
+    float* xch = stage + 2 * G::kStageFloats;
+    uint64_t* full = reinterpret_cast<uint64_t*>(xch + G::kXchFloats);
+    uint64_t* empty = full + 2;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        mbar_init(&full[0], 1);
+        mbar_init(&full[1], 1);
+        mbar_init(&empty[0], NW);
+        mbar_init(&empty[1], NW);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    if (warp == NW) {
+        // ---------------- producer warp: TMA tile stream ----------------
+        if (lane == 0) {
+            for (int i = 0, t = blockIdx.x; t < a.ntiles; t += gridDim.x, ++i) {
+                const int s = i & 1;
+                if (i >= 2) mbar_wait(&empty[s], ((i >> 1) - 1) & 1);
+                const int ty = t / a.tiles_x, tx = t - ty * a.tiles_x;
+                const int cx = a.X0 + tx * a.TW - H;      // first compute cell column
+                const int cy = a.Y0 + ty * a.TH - H - 1;  // ghost row above the region
+                float* dst = stage + s * G::kStageFloats;
+                mbar_expect_tx(&full[s], G::kStageBytes);
+                if (DIR == 0) {
+                    tma_load_2d(dst, &m0, &full[s], 2 * cx, 2 * cy);
+                } else {
+                    constexpr int plane = TWC * G::kRows;
+                    tma_load_2d(dst, &m0, &full[s], cx, cy);
+                    tma_load_2d(dst + plane, &m1, &full[s], cx, cy);
+                    tma_load_2d(dst + 2 * plane, &m2, &full[s], cx, cy);
+                    tma_load_2d(dst + 3 * plane, &m3, &full[s], cx, cy);
+                }
+            }
+        }
+        return;
+    }
+
+    // ---------------- compute warps ----------------
+    float v[R][CPT][4];
+    float gu[CPT][4], gd[CPT][4];
+    int xslot = 0;
+
+    for (int i = 0, t = blockIdx.x; t < a.ntiles; t += gridDim.x, ++i) {
+        const int s = i & 1;
+        mbar_wait(&full[s], (i >> 1) & 1);
+        const float* st = stage + s * G::kStageFloats;
+
+        // Load the warp's rows (+ one ghost row above and below) and split
+        // the 2x2 polyphase components.
+        auto load_row = [&](int q, float (&dst)[CPT][4]) {
+            // q: cell row in the stage (0 = ghost row above the region)
+            if (DIR == 0) {
+                const float* p0 = st + (2 * q) * (2 * TWC) + 4 * lane;
+                const float4 e = *reinterpret_cast<const float4*>(p0);
+                const float4 o = *reinterpret_cast<const float4*>(p0 + 2 * TWC);
+                dst[0][0] = e.x; dst[0][1] = e.y; dst[0][2] = o.x; dst[0][3] = o.y;
+                dst[1][0] = e.z; dst[1][1] = e.w; dst[1][2] = o.z; dst[1][3] = o.w;
+            } else {
+                constexpr int plane = TWC * G::kRows;
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const float2 p =
+                        *reinterpret_cast<const float2*>(st + c * plane + q * TWC + 2 * lane);
+                    dst[0][c] = p.x;
+                    dst[1][c] = p.y;
+                }
+            }
+        };
+        load_row(warp * R, gu);
+#pragma unroll
+        for (int r = 0; r < R; ++r) load_row(warp * R + 1 + r, v[r]);
+        load_row(warp * R + R + 1, gd);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+
+        if (DIR == 1 && a.scaling) {  // undo scaling first (transform.cpp:180)
+#pragma unroll
+            for (int c = 0; c < CPT; ++c) {
+                gu[c][0] *= a.scale; gu[c][3] /= a.scale;
+                gd[c][0] *= a.scale; gd[c][3] /= a.scale;
+#pragma unroll
+                for (int r = 0; r < R; ++r) { v[r][c][0] *= a.scale; v[r][c][3] /= a.scale; }
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < CPT; ++c) {
+            P::pre(gu[c]);
+            P::pre(gd[c]);
+#pragma unroll
+            for (int r = 0; r < R; ++r) P::pre(v[r][c]);
+        }
+
+        sfor<P::kEpochs>([&](auto e_) {
+            constexpr int E = decltype(e_)::value;
+            constexpr unsigned long long U = P::kUse[E];
+            if constexpr (E > 0) {
+                // Publish edge rows, one block barrier, fetch neighbours'.
+                float* x = xch + ((xslot * NW + warp) * 2) * (32 * CPT * 4);
+                float4* top = reinterpret_cast<float4*>(x + lane * CPT * 4);
+                float4* bot = reinterpret_cast<float4*>(x + 32 * CPT * 4 + lane * CPT * 4);
+#pragma unroll
+                for (int c = 0; c < CPT; ++c) {
+                    top[c] = make_float4(v[0][c][0], v[0][c][1], v[0][c][2], v[0][c][3]);
+                    bot[c] = make_float4(v[R - 1][c][0], v[R - 1][c][1], v[R - 1][c][2],
+                                         v[R - 1][c][3]);
+                }
+                named_sync(1, NW * 32);
+                if (warp > 0) {
+                    const float4* nb = reinterpret_cast<const float4*>(
+                        x - 2 * 32 * CPT * 4 + 32 * CPT * 4 + lane * CPT * 4);
+#pragma unroll
+                    for (int c = 0; c < CPT; ++c) {
+                        const float4 q = nb[c];
+                        gu[c][0] = q.x; gu[c][1] = q.y; gu[c][2] = q.z; gu[c][3] = q.w;
+                    }
+                }
+                if (warp < NW - 1) {
+                    const float4* nb =
+                        reinterpret_cast<const float4*>(x + 2 * 32 * CPT * 4 + lane * CPT * 4);
+#pragma unroll
+                    for (int c = 0; c < CPT; ++c) {
+                        const float4 q = nb[c];
+                        gd[c][0] = q.x; gd[c][1] = q.y; gd[c][2] = q.z; gd[c][3] = q.w;
+                    }
+                }
+                xslot ^= 1;
+            }
+            // Horizontal neighbours of the lane's edge columns (warp shuffle).
+            float sl[R + 2][4], sr[R + 2][4];
+            sfor<4>([&](auto c_) {
+                constexpr int C = decltype(c_)::value;
+                if constexpr (uses_dc(U, C, -1)) {
+                    if constexpr (uses(U, C, -1, -1))
+                        sl[0][C] = __shfl_up_sync(0xffffffffu, gu[CPT - 1][C], 1);
+#pragma unroll
+                    for (int r = 0; r < R; ++r)
+                        sl[r + 1][C] = __shfl_up_sync(0xffffffffu, v[r][CPT - 1][C], 1);
+                    if constexpr (uses(U, C, 1, -1))
+                        sl[R + 1][C] = __shfl_up_sync(0xffffffffu, gd[CPT - 1][C], 1);
+                }
+                if constexpr (uses_dc(U, C, 1)) {
+                    if constexpr (uses(U, C, -1, 1))
+                        sr[0][C] = __shfl_down_sync(0xffffffffu, gu[0][C], 1);
+#pragma unroll
+                    for (int r = 0; r < R; ++r)
+                        sr[r + 1][C] = __shfl_down_sync(0xffffffffu, v[r][0][C], 1);
+                    if constexpr (uses(U, C, 1, 1))
+                        sr[R + 1][C] = __shfl_down_sync(0xffffffffu, gd[0][C], 1);
+                }
+            });
+            float o[R][CPT][4];
+            sfor<R>([&](auto r_) {
+                sfor<CPT>([&](auto c_) {
+                    constexpr int RR = decltype(r_)::value, CC = decltype(c_)::value;
+                    Acc<R, RR, CC> acc{v, gu, gd, sl, sr};
+                    P::template nbr<E>(acc, o[RR][CC]);
+                });
+            });
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+#pragma unroll
+                for (int c = 0; c < CPT; ++c) {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) v[r][c][k] = o[r][c][k];
+                    P::template post<E>(v[r][c]);
+                }
+        });
+
+        // ---------------- store ----------------
+        const int ty = t / a.tiles_x, tx = t - ty * a.tiles_x;
+        const int gy0 = a.Y0 + ty * a.TH - H + warp * R;  // global cell row of v[0]
+        const int gx = a.X0 + tx * a.TW - H + CPT * lane;  // global cell col of column 0
+        const bool c0 = CPT * lane >= H && CPT * lane < H + a.TW;
+        const bool c1 = CPT * lane + 1 >= H && CPT * lane + 1 < H + a.TW;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int qr = warp * R + r;
+            if (qr < H || qr >= NW * R - H) continue;
+            const int gy = gy0 + r;
+            if (DIR == 0) {
+                float lo[4] = {v[r][0][0], v[r][0][1], v[r][0][2], v[r][0][3]};
+                float hi[4] = {v[r][1][0], v[r][1][1], v[r][1][2], v[r][1][3]};
+                if (a.scaling) {  // scale_planes (transform.cpp:154-159)
+                    lo[0] *= a.scale; lo[3] /= a.scale;
+                    hi[0] *= a.scale; hi[3] /= a.scale;
+                }
+                const long off = (long)gy * a.out_pitch + gx;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    float* p = a.out[k] + off;
+                    if (c0 && c1)
+                        *reinterpret_cast<float2*>(p) = make_float2(lo[k], hi[k]);
+                    else if (c0)
+                        p[0] = lo[k];
+                    else if (c1)
+                        p[1] = hi[k];
+                }
+            } else {
+                float* p0 = a.out[0] + (long)(2 * gy) * a.out_pitch + 2 * gx;
+                float* p1 = p0 + a.out_pitch;
+                if (c0 && c1) {
+                    *reinterpret_cast<float4*>(p0) =
+                        make_float4(v[r][0][0], v[r][0][1], v[r][1][0], v[r][1][1]);
+                    *reinterpret_cast<float4*>(p1) =
+                        make_float4(v[r][0][2], v[r][0][3], v[r][1][2], v[r][1][3]);
+                } else if (c0) {
+                    *reinterpret_cast<float2*>(p0) = make_float2(v[r][0][0], v[r][0][1]);
+                    *reinterpret_cast<float2*>(p1) = make_float2(v[r][0][2], v[r][0][3]);
+                } else if (c1) {
+                    *reinterpret_cast<float2*>(p0 + 2) = make_float2(v[r][1][0], v[r][1][1]);
+                    *reinterpret_cast<float2*>(p1 + 2) = make_float2(v[r][1][2], v[r][1][3]);
+                }
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------------ host side
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_fn();
+
+bool make_map(CUtensorMap* m, const float* base, int w, int h, long pitch, int box_w, int box_h);
+
+// Launch configuration per wavelet: (R, NW).
+template <int WAVELET>
+struct Config;
+template <>
+struct Config<0> {  // cdf53, halo 1
+    static constexpr int R = 4, NW = 8;
+};
+template <>
+struct Config<1> {  // cdf97, halo 2
+    static constexpr int R = 4, NW = 8;
+};
+
+struct Plan {
+    FastArgs args;
+    int tiles_y;
+    bool ok;
+};
+
+// Tile grid of the fast path; the rest of the image is the interpreter's frame.
+inline Plan plan_tiles(const WlLevel& L, int H, int R, int NW) {
+    Plan p{};
+    // TMA requires the innermost box start to be 16-byte aligned: the inverse
+    // boxes start at cell column X0 - H + tx*TW of a float32 plane, so TW is
+    // rounded down to a multiple of 4 there (the forward starts at pixel
+    // column 2*(...) and 2*(64 - 2H) is a multiple of 4 for H = 1, 2).
+    const int TW = L.direction == 0 ? TWC - 2 * H : ((TWC - 2 * H) & ~3);
+    const int TH = NW * R - 2 * H;
+    const int X0 = H, Y0 = H + 1;
+    const int tx = L.qw >= TWC ? (L.qw - TWC) / TW + 1 : 0;
+    const int span = L.qh - (Y0 - H - 1);  // rows available from the first ghost row
+    const int ty = span >= NW * R + 2 ? (span - (NW * R + 2)) / TH + 1 : 0;
+    p.args.tiles_x = tx;
+    p.tiles_y = ty;
+    p.args.ntiles = tx * ty;
+    p.args.X0 = X0;
+    p.args.Y0 = Y0;
+    p.args.TW = TW;
+    p.args.TH = TH;
+    p.ok = tx > 0 && ty > 0;
+    return p;
+}
+
+template <class P, int DIR, int R, int NW>
+cudaError_t launch(const WlLevel& L, const Plan& plan, cudaStream_t stream) {
+    using G = Geometry<R, NW>;
+    CUtensorMap maps[4];
+    FastArgs a = plan.args;
+    if (DIR == 0) {
+        if (!make_map(&maps[0], L.in[0], 2 * L.qw, 2 * L.qh, L.in_pitch, 2 * TWC, 2 * G::kRows))
+            return cudaErrorInvalidValue;
+        maps[1] = maps[2] = maps[3] = maps[0];
+        for (int k = 0; k < 4; ++k) a.out[k] = L.out[k];
+    } else {
+        for (int k = 0; k < 4; ++k)
+            if (!make_map(&maps[k], L.in[k], L.qw, L.qh, L.in_pitch, TWC, G::kRows))
+                return cudaErrorInvalidValue;
+        a.out[0] = L.out[0];
+        a.out[1] = a.out[2] = a.out[3] = nullptr;
+        if (getenv("WL_DBG_TMA")) maps[1] = maps[2] = maps[3] = maps[0];
+    }
+    a.out_pitch = L.out_pitch;
+    a.scaling = L.scaling && wl_host_program(L.prog).has_scale;
+    a.scale = wl_host_program(L.prog).scale;
+    auto kern = fast_kernel<P, DIR, R, NW>;
+    static int max_blocks[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int& mb = max_blocks[dev & 63];
+    if (mb == 0) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)G::kSmemBytes);
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (NW + 1) * 32,
+                                                      G::kSmemBytes);
+        int sms = 0;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        mb = (per_sm > 0 ? per_sm : 1) * sms;
+    }
+    const int grid = a.ntiles < mb ? a.ntiles : mb;
+    kern<<<grid, (NW + 1) * 32, G::kSmemBytes, stream>>>(maps[0], maps[1], maps[2], maps[3], a);
+    wl_count_launch();
+    return cudaGetLastError();
+}
+
+}  // namespace wlfast

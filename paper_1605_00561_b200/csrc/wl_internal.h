@@ -21,8 +21,16 @@ struct WlLevel {
 const WlProgram& wl_host_program(int prog);
 const WlStep* wl_host_steps();
 
+// Up to 4 rectangles of output cells (the frame around the fast engine's
+// tile grid); one CTA per 32x32 tile of each rectangle.
+struct WlRects {
+    int n;
+    int y0[4], x0[4], ny[4], nx[4];
+};
+
 // Generic tile interpreter: every wavelet/scheme/direction/boundary.
 cudaError_t wl_launch_interp(const WlLevel& L, cudaStream_t stream);
+cudaError_t wl_launch_interp_rects(const WlLevel& L, const WlRects& R, cudaStream_t stream);
 // Direct 2-D convolution forward (SchemeKind::Convolution).
 cudaError_t wl_launch_conv(const WlLevel& L, cudaStream_t stream);
 // Fast register-tile engine; returns cudaErrorNotSupported when the

@@ -30,7 +30,7 @@ namespace {
 
 constexpr int TQ = 32;        // output cells per tile side
 constexpr int NT = 256;       // threads per CTA
-constexpr int MAXH = 3;       // largest program halo (dd137)
+constexpr int MAXH = 6;       // largest tile halo: 2 x dd137's reach (symmetric)
 constexpr int RSMAX = TQ + 2 * MAXH;
 constexpr int K = (RSMAX * RSMAX + NT - 1) / NT;  // cells per thread
 
@@ -59,14 +59,28 @@ __device__ __forceinline__ float pick(const float (&v)[4], int i) {
 }
 
 template <int DIR>
-__global__ void __launch_bounds__(NT) interp_kernel(const WlLevel L) {
+__global__ void __launch_bounds__(NT) interp_kernel(const WlLevel L, const WlRects RC) {
     extern __shared__ float sm[];
     const WlProgram& P = c_progs[L.prog];
-    const int H = P.halo;
+    const bool sym = L.boundary == 1;
+    // Symmetric: a read past the image border is mirrored back inwards, so
+    // next to a border the up- and down-reach (left and right) add up.
+    const int H = sym ? 2 * P.halo : P.halo;
     const int RS = TQ + 2 * H;
     const int plane = RS * RS;
-    const int oy = blockIdx.y * TQ - H, ox = blockIdx.x * TQ - H;
-    const bool sym = L.boundary == 1;
+    // Linear block index -> (rectangle, tile) of the output region.
+    int b = blockIdx.x, rect = 0;
+    int tiles_x = (RC.nx[0] + TQ - 1) / TQ;
+    while (rect + 1 < RC.n && b >= tiles_x * ((RC.ny[rect] + TQ - 1) / TQ)) {
+        b -= tiles_x * ((RC.ny[rect] + TQ - 1) / TQ);
+        ++rect;
+        tiles_x = (RC.nx[rect] + TQ - 1) / TQ;
+    }
+    const int ty = b / tiles_x, tx = b - (b / tiles_x) * tiles_x;
+    const int ry0 = RC.y0[rect] + ty * TQ, rx0 = RC.x0[rect] + tx * TQ;  // tile output origin
+    const int ry1 = min(ry0 + TQ, RC.y0[rect] + RC.ny[rect]);
+    const int rx1 = min(rx0 + TQ, RC.x0[rect] + RC.nx[rect]);
+    const int oy = ry0 - H, ox = rx0 - H;
 
     float v[K][4];
     int ly[K], lx[K];
@@ -164,8 +178,8 @@ __global__ void __launch_bounds__(NT) interp_kernel(const WlLevel L) {
 #pragma unroll
     for (int k = 0; k < K; ++k) {
         const int gy = oy + ly[k], gx = ox + lx[k];
-        if (!live[k] || ly[k] < H || ly[k] >= H + TQ || lx[k] < H || lx[k] >= H + TQ ||
-            gy >= L.qh || gx >= L.qw)
+        if (!live[k] || gy < ry0 || gy >= ry1 || gx < rx0 || gx >= rx1 || gy >= L.qh ||
+            gx >= L.qw)
             continue;
         if (DIR == 0) {
             if (L.scaling && P.has_scale) {  // scale_planes (transform.cpp:154-159)
@@ -240,10 +254,31 @@ const WlProgram& wl_host_program(int prog) { return h_progs[prog]; }
 const WlStep* wl_host_steps() { return h_steps; }
 
 cudaError_t wl_launch_interp(const WlLevel& L, cudaStream_t stream) {
+    WlRects R{};
+    R.n = 1;
+    R.ny[0] = L.qh;
+    R.nx[0] = L.qw;
+    return wl_launch_interp_rects(L, R, stream);
+}
+
+cudaError_t wl_launch_interp_rects(const WlLevel& L, const WlRects& RC, cudaStream_t stream) {
     const WlProgram& P = h_progs[L.prog];
-    const int RS = TQ + 2 * P.halo;
+    const int RS = TQ + 2 * (L.boundary == 1 ? 2 * P.halo : P.halo);
     const size_t smem = 2 * 4 * (size_t)RS * RS * sizeof(float);
-    const dim3 grid((L.qw + TQ - 1) / TQ, (L.qh + TQ - 1) / TQ);
+    // Drop empty rectangles; one CTA per 32x32 tile of each remaining one.
+    WlRects R{};
+    long blocks = 0;
+    for (int i = 0; i < RC.n; ++i) {
+        if (RC.ny[i] <= 0 || RC.nx[i] <= 0) continue;
+        R.y0[R.n] = RC.y0[i];
+        R.x0[R.n] = RC.x0[i];
+        R.ny[R.n] = RC.ny[i];
+        R.nx[R.n] = RC.nx[i];
+        blocks += (long)((RC.ny[i] + TQ - 1) / TQ) * ((RC.nx[i] + TQ - 1) / TQ);
+        ++R.n;
+    }
+    if (R.n == 0) return cudaSuccess;
+    const dim3 grid((unsigned)blocks);
     static bool attr_set[64] = {};
     int dev = 0;
     cudaGetDevice(&dev);
@@ -256,9 +291,9 @@ cudaError_t wl_launch_interp(const WlLevel& L, cudaStream_t stream) {
         attr_set[dev & 63] = true;
     }
     if (L.direction == 0)
-        interp_kernel<0><<<grid, NT, smem, stream>>>(L);
+        interp_kernel<0><<<grid, NT, smem, stream>>>(L, R);
     else
-        interp_kernel<1><<<grid, NT, smem, stream>>>(L);
+        interp_kernel<1><<<grid, NT, smem, stream>>>(L, R);
     wl_count_launch();
     return cudaGetLastError();
 }
