@@ -42,11 +42,11 @@ int launch_level(WlLevel L, cudaStream_t s) {
     }
     const WlProgram& P = wl_host_program(L.prog);
     cudaError_t e;
+    const int engine = g_engine.load();
     if (P.is_conv) {
-        e = wl_launch_conv(L, s);
+        e = (engine != 1 && L.wavelet <= 1) ? wl_launch_conv_fast(L, s) : wl_launch_conv(L, s);
         return cuda_status(e, "conv_kernel");
     }
-    const int engine = g_engine.load();
     if (engine == 2 && !wl_fast_supported(L))
         return fail(WL_EINVAL, "fast engine does not support this wavelet/scheme");
     if (engine != 1 && wl_fast_supported(L)) {

@@ -160,8 +160,8 @@ __global__ void __launch_bounds__((NW + 1) * 32)
     if (threadIdx.x == 0) {
         mbar_init(&full[0], 1);
         mbar_init(&full[1], 1);
-        mbar_init(&empty[0], NW);
-        mbar_init(&empty[1], NW);
+        mbar_init(&empty[0], NW * 32);
+        mbar_init(&empty[1], NW * 32);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -226,8 +226,13 @@ __global__ void __launch_bounds__((NW + 1) * 32)
 #pragma unroll
         for (int r = 0; r < R; ++r) load_row(warp * R + 1 + r, v[r]);
         load_row(warp * R + R + 1, gd);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[s]);
+        // Release the stage: every lane's own loads are ordered before its
+        // arrive (release semantics; a single elected arrive after __syncwarp
+        // let the next TMA overwrite rows other lanes had not finished
+        // reading), and the proxy fence orders these generic-proxy reads
+        // before the async-proxy (TMA) writes of the refill.
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive(&empty[s]);
 
         if (DIR == 1 && a.scaling) {  // undo scaling first (transform.cpp:180)
 #pragma unroll

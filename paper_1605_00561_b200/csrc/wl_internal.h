@@ -26,13 +26,16 @@ const WlStep* wl_host_steps();
 struct WlRects {
     int n;
     int y0[4], x0[4], ny[4], nx[4];
+    int ty[4], tx[4];  // tile shape per rectangle (set by wl_launch_interp_rects)
 };
 
 // Generic tile interpreter: every wavelet/scheme/direction/boundary.
 cudaError_t wl_launch_interp(const WlLevel& L, cudaStream_t stream);
 cudaError_t wl_launch_interp_rects(const WlLevel& L, const WlRects& R, cudaStream_t stream);
-// Direct 2-D convolution forward (SchemeKind::Convolution).
+// Direct 2-D convolution forward (SchemeKind::Convolution): generic
+// (every wavelet) and the register/TMA kernel for cdf53/cdf97.
 cudaError_t wl_launch_conv(const WlLevel& L, cudaStream_t stream);
+cudaError_t wl_launch_conv_fast(const WlLevel& L, cudaStream_t stream);
 // Fast register-tile engine; returns cudaErrorNotSupported when the
 // (wavelet, scheme, direction) has no fast instantiation.
 cudaError_t wl_launch_fast(const WlLevel& L, cudaStream_t stream);

@@ -66,20 +66,23 @@ __global__ void __launch_bounds__(NT) interp_kernel(const WlLevel L, const WlRec
     // Symmetric: a read past the image border is mirrored back inwards, so
     // next to a border the up- and down-reach (left and right) add up.
     const int H = sym ? 2 * P.halo : P.halo;
-    const int RS = TQ + 2 * H;
-    const int plane = RS * RS;
-    // Linear block index -> (rectangle, tile) of the output region.
+    // Linear block index -> (rectangle, tile) of the output region; each
+    // rectangle has its own tile shape (TY x TX output cells; thin frame
+    // strips get flat tiles so little work is spent on discarded halo).
     int b = blockIdx.x, rect = 0;
-    int tiles_x = (RC.nx[0] + TQ - 1) / TQ;
-    while (rect + 1 < RC.n && b >= tiles_x * ((RC.ny[rect] + TQ - 1) / TQ)) {
-        b -= tiles_x * ((RC.ny[rect] + TQ - 1) / TQ);
+    int tiles_x = (RC.nx[0] + RC.tx[0] - 1) / RC.tx[0];
+    while (rect + 1 < RC.n && b >= tiles_x * ((RC.ny[rect] + RC.ty[rect] - 1) / RC.ty[rect])) {
+        b -= tiles_x * ((RC.ny[rect] + RC.ty[rect] - 1) / RC.ty[rect]);
         ++rect;
-        tiles_x = (RC.nx[rect] + TQ - 1) / TQ;
+        tiles_x = (RC.nx[rect] + RC.tx[rect] - 1) / RC.tx[rect];
     }
+    const int TY = RC.ty[rect], TX = RC.tx[rect];
+    const int RSY = TY + 2 * H, RS = TX + 2 * H;  // region rows, region row length
+    const int plane = RSY * RS;
     const int ty = b / tiles_x, tx = b - (b / tiles_x) * tiles_x;
-    const int ry0 = RC.y0[rect] + ty * TQ, rx0 = RC.x0[rect] + tx * TQ;  // tile output origin
-    const int ry1 = min(ry0 + TQ, RC.y0[rect] + RC.ny[rect]);
-    const int rx1 = min(rx0 + TQ, RC.x0[rect] + RC.nx[rect]);
+    const int ry0 = RC.y0[rect] + ty * TY, rx0 = RC.x0[rect] + tx * TX;  // tile output origin
+    const int ry1 = min(ry0 + TY, RC.y0[rect] + RC.ny[rect]);
+    const int rx1 = min(rx0 + TX, RC.x0[rect] + RC.nx[rect]);
     const int oy = ry0 - H, ox = rx0 - H;
 
     float v[K][4];
@@ -145,7 +148,7 @@ __global__ void __launch_bounds__(NT) interp_kernel(const WlLevel L, const WlRec
                             if (gy < 0 || gy >= L.qh) yy = resolve(gy, L.qh, 1) - oy;
                             if (gx < 0 || gx >= L.qw) xx = resolve(gx, L.qw, 1) - ox;
                         }
-                        yy = min(max(yy, 0), RS - 1);
+                        yy = min(max(yy, 0), RSY - 1);
                         xx = min(max(xx, 0), RS - 1);
                         acc = fmaf(tp.c, b[tp.src * plane + yy * RS + xx], acc);
                     }
@@ -258,32 +261,48 @@ cudaError_t wl_launch_interp(const WlLevel& L, cudaStream_t stream) {
     R.n = 1;
     R.ny[0] = L.qh;
     R.nx[0] = L.qw;
+    R.ty[0] = R.tx[0] = TQ;
     return wl_launch_interp_rects(L, R, stream);
 }
 
 cudaError_t wl_launch_interp_rects(const WlLevel& L, const WlRects& RC, cudaStream_t stream) {
     const WlProgram& P = h_progs[L.prog];
-    const int RS = TQ + 2 * (L.boundary == 1 ? 2 * P.halo : P.halo);
-    const size_t smem = 2 * 4 * (size_t)RS * RS * sizeof(float);
-    // Drop empty rectangles; one CTA per 32x32 tile of each remaining one.
+    const int H = L.boundary == 1 ? 2 * P.halo : P.halo;
+    const int cap = NT * K;  // region cells one CTA holds
+    // Drop empty rectangles and pick a tile shape per rectangle: 32x32 in
+    // general, flat tiles for thin strips (the frame around the fast engine).
     WlRects R{};
     long blocks = 0;
+    size_t cells = 0;
     for (int i = 0; i < RC.n; ++i) {
         if (RC.ny[i] <= 0 || RC.nx[i] <= 0) continue;
+        int ty = TQ, tx = TQ;
+        if (RC.ny[i] < TQ && RC.ny[i] <= RC.nx[i]) {
+            ty = RC.ny[i];
+            tx = cap / (ty + 2 * H) - 2 * H;
+        } else if (RC.nx[i] < TQ) {
+            tx = RC.nx[i];
+            ty = cap / (tx + 2 * H) - 2 * H;
+        }
         R.y0[R.n] = RC.y0[i];
         R.x0[R.n] = RC.x0[i];
         R.ny[R.n] = RC.ny[i];
         R.nx[R.n] = RC.nx[i];
-        blocks += (long)((RC.ny[i] + TQ - 1) / TQ) * ((RC.nx[i] + TQ - 1) / TQ);
+        R.ty[R.n] = ty;
+        R.tx[R.n] = tx;
+        const size_t c = (size_t)(ty + 2 * H) * (tx + 2 * H);
+        cells = c > cells ? c : cells;
+        blocks += (long)((RC.ny[i] + ty - 1) / ty) * ((RC.nx[i] + tx - 1) / tx);
         ++R.n;
     }
     if (R.n == 0) return cudaSuccess;
+    const size_t smem = 2 * 4 * cells * sizeof(float);
     const dim3 grid((unsigned)blocks);
     static bool attr_set[64] = {};
     int dev = 0;
     cudaGetDevice(&dev);
     if (!attr_set[dev & 63]) {
-        const size_t maxsm = 2 * 4 * (size_t)RSMAX * RSMAX * sizeof(float);
+        const size_t maxsm = 2 * 4 * (size_t)cap * sizeof(float);
         cudaFuncSetAttribute(interp_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)maxsm);
         cudaFuncSetAttribute(interp_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
