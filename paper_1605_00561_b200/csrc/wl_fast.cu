@@ -96,8 +96,9 @@ cudaError_t wl_launch_fast(const WlLevel& L, cudaStream_t stream) {
         e = L.direction == 0 ? wl_fast_cdf97_fwd(L.scheme, L, plan, stream)
                              : wl_fast_cdf97_inv(L.scheme, L, plan, stream);
     if (e != cudaSuccess) return e;
-    // The frame around the tile grid (image borders included) goes to the
-    // interpreter, which resolves boundaries exactly per step.
+    if (plan.args.wrap) return cudaSuccess;  // periodic: the grid covers the image
+    // Symmetric: the frame around the tile grid (image borders included) goes
+    // to the interpreter, which mirrors every out-of-image read per step.
     const int Y0 = plan.args.Y0, X0 = plan.args.X0;
     const int Y1 = Y0 + plan.tiles_y * plan.args.TH, X1 = X0 + plan.args.tiles_x * plan.args.TW;
     WlRects fr{};

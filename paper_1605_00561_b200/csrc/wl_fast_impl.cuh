@@ -89,11 +89,16 @@ __device__ __forceinline__ void named_sync(int id, int nthreads) {
 }
 
 struct FastArgs {
-    float* out[4];   // fwd: LL, HL, LH, HH planes; inv: out[0] = image
-    long out_pitch;  // elements
+    const float* in[4];  // fwd: in[0] = image; inv: LL, HL, LH, HH (wrapped border loads)
+    long in_pitch;
+    float* out[4];       // fwd: LL, HL, LH, HH planes; inv: out[0] = image
+    long out_pitch;      // elements
+    int qw, qh;          // component-grid size
     int tiles_x, ntiles;
-    int X0, Y0;      // first output cell of tile (0, 0)
-    int TW, TH;      // output tile size in cells
+    int t0;              // index of the first tile row/column (-1 when covering borders)
+    int X0, Y0;          // first output cell of tile (0, 0)
+    int TW, TH;          // output tile size in cells
+    int wrap;            // periodic plan covering the whole image (border tiles wrap)
     int scaling;
     float scale;
 };
@@ -172,7 +177,8 @@ __global__ void __launch_bounds__((NW + 1) * 32)
             for (int i = 0, t = blockIdx.x; t < a.ntiles; t += gridDim.x, ++i) {
                 const int s = i & 1;
                 if (i >= 2) mbar_wait(&empty[s], ((i >> 1) - 1) & 1);
-                const int ty = t / a.tiles_x, tx = t - ty * a.tiles_x;
+                const int tyi = t / a.tiles_x;
+                const int ty = tyi + a.t0, tx = t - tyi * a.tiles_x + a.t0;
                 const int cx = a.X0 + tx * a.TW - H;      // first compute cell column
                 const int cy = a.Y0 + ty * a.TH - H - 1;  // ghost row above the region
                 float* dst = stage + s * G::kStageFloats;
@@ -198,6 +204,15 @@ __global__ void __launch_bounds__((NW + 1) * 32)
 
     for (int i = 0, t = blockIdx.x; t < a.ntiles; t += gridDim.x, ++i) {
         const int s = i & 1;
+        const int tyi = t / a.tiles_x;
+        const int ty = tyi + a.t0, tx = t - tyi * a.tiles_x + a.t0;
+        const int cx = a.X0 + tx * a.TW - H;      // first compute cell column
+        const int cy = a.Y0 + ty * a.TH - H - 1;  // ghost row above the region
+        // Periodic border tile (only when the plan covers the whole image):
+        // its cells are loaded with wrapped coordinates straight from global
+        // memory -- load-time wrap is exact for the periodic extension.
+        const bool wrap_tile =
+            a.wrap && (cx < 0 || cy < 0 || cx + TWC > a.qw || cy + G::kRows > a.qh);
         mbar_wait(&full[s], (i >> 1) & 1);
         const float* st = stage + s * G::kStageFloats;
 
@@ -205,7 +220,25 @@ __global__ void __launch_bounds__((NW + 1) * 32)
         // the 2x2 polyphase components.
         auto load_row = [&](int q, float (&dst)[CPT][4]) {
             // q: cell row in the stage (0 = ghost row above the region)
-            if (DIR == 0) {
+            if (wrap_tile) {
+                int ry = (cy + q) % a.qh;
+                ry += ry < 0 ? a.qh : 0;
+#pragma unroll
+                for (int j = 0; j < CPT; ++j) {
+                    int rx = (cx + CPT * lane + j) % a.qw;
+                    rx += rx < 0 ? a.qw : 0;
+                    if (DIR == 0) {
+                        const float* p = a.in[0] + (long)(2 * ry) * a.in_pitch + 2 * rx;
+                        dst[j][0] = p[0];
+                        dst[j][1] = p[1];
+                        dst[j][2] = p[a.in_pitch];
+                        dst[j][3] = p[a.in_pitch + 1];
+                    } else {
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) dst[j][c] = a.in[c][(long)ry * a.in_pitch + rx];
+                    }
+                }
+            } else if (DIR == 0) {
                 const float* p0 = st + (2 * q) * (2 * TWC) + 4 * lane;
                 const float4 e = *reinterpret_cast<const float4*>(p0);
                 const float4 o = *reinterpret_cast<const float4*>(p0 + 2 * TWC);
@@ -328,16 +361,17 @@ __global__ void __launch_bounds__((NW + 1) * 32)
         });
 
         // ---------------- store ----------------
-        const int ty = t / a.tiles_x, tx = t - ty * a.tiles_x;
-        const int gy0 = a.Y0 + ty * a.TH - H + warp * R;  // global cell row of v[0]
-        const int gx = a.X0 + tx * a.TW - H + CPT * lane;  // global cell col of column 0
-        const bool c0 = CPT * lane >= H && CPT * lane < H + a.TW;
-        const bool c1 = CPT * lane + 1 >= H && CPT * lane + 1 < H + a.TW;
+        const int gy0 = cy + 1 + warp * R;  // global cell row of v[0]
+        const int gx = cx + CPT * lane;     // global cell col of column 0
+        // output columns of this tile, clipped to the image (partial tiles)
+        const bool c0 = CPT * lane >= H && CPT * lane < H + a.TW && gx >= 0 && gx < a.qw;
+        const bool c1 =
+            CPT * lane + 1 >= H && CPT * lane + 1 < H + a.TW && gx + 1 >= 0 && gx + 1 < a.qw;
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             const int qr = warp * R + r;
-            if (qr < H || qr >= NW * R - H) continue;
             const int gy = gy0 + r;
+            if (qr < H || qr >= H + a.TH || gy < 0 || gy >= a.qh) continue;
             if (DIR == 0) {
                 float lo[4] = {v[r][0][0], v[r][0][1], v[r][0][2], v[r][0][3]};
                 float hi[4] = {v[r][1][0], v[r][1][1], v[r][1][2], v[r][1][3]};
@@ -403,7 +437,11 @@ struct Plan {
     bool ok;
 };
 
-// Tile grid of the fast path; the rest of the image is the interpreter's frame.
+// Tile grid of the fast path.
+//  * periodic: the grid covers the whole image (one extra tile row/column on
+//    the top/left, t0 = -1); border tiles load wrapped cells (exact).
+//  * symmetric: only tiles whose compute region lies inside the image; the
+//    frame around them is the interpreter's (per-step mirroring).
 inline Plan plan_tiles(const WlLevel& L, int H, int R, int NW) {
     Plan p{};
     // TMA requires the innermost box start to be 16-byte aligned: the inverse
@@ -413,9 +451,19 @@ inline Plan plan_tiles(const WlLevel& L, int H, int R, int NW) {
     const int TW = L.direction == 0 ? TWC - 2 * H : ((TWC - 2 * H) & ~3);
     const int TH = NW * R - 2 * H;
     const int X0 = H, Y0 = H + 1;
-    const int tx = L.qw >= TWC ? (L.qw - TWC) / TW + 1 : 0;
-    const int span = L.qh - (Y0 - H - 1);  // rows available from the first ghost row
-    const int ty = span >= NW * R + 2 ? (span - (NW * R + 2)) / TH + 1 : 0;
+    int tx, ty;
+    if (L.boundary == 0) {
+        tx = (L.qw - X0 > 0 ? (L.qw - X0 + TW - 1) / TW : 0) + 1;
+        ty = (L.qh - Y0 > 0 ? (L.qh - Y0 + TH - 1) / TH : 0) + 1;
+        p.args.t0 = -1;
+        p.args.wrap = 1;
+    } else {
+        tx = L.qw >= TWC ? (L.qw - TWC) / TW + 1 : 0;
+        const int span = L.qh - (Y0 - H - 1);  // rows available from the first ghost row
+        ty = span >= NW * R + 2 ? (span - (NW * R + 2)) / TH + 1 : 0;
+        p.args.t0 = 0;
+        p.args.wrap = 0;
+    }
     p.args.tiles_x = tx;
     p.tiles_y = ty;
     p.args.ntiles = tx * ty;
@@ -423,6 +471,8 @@ inline Plan plan_tiles(const WlLevel& L, int H, int R, int NW) {
     p.args.Y0 = Y0;
     p.args.TW = TW;
     p.args.TH = TH;
+    p.args.qw = L.qw;
+    p.args.qh = L.qh;
     p.ok = tx > 0 && ty > 0;
     return p;
 }
@@ -443,8 +493,9 @@ cudaError_t launch(const WlLevel& L, const Plan& plan, cudaStream_t stream) {
                 return cudaErrorInvalidValue;
         a.out[0] = L.out[0];
         a.out[1] = a.out[2] = a.out[3] = nullptr;
-        if (getenv("WL_DBG_TMA")) maps[1] = maps[2] = maps[3] = maps[0];
     }
+    for (int k = 0; k < 4; ++k) a.in[k] = L.in[k];
+    a.in_pitch = L.in_pitch;
     a.out_pitch = L.out_pitch;
     a.scaling = L.scaling && wl_host_program(L.prog).has_scale;
     a.scale = wl_host_program(L.prog).scale;

@@ -279,10 +279,12 @@ cudaError_t wl_launch_interp_rects(const WlLevel& L, const WlRects& RC, cudaStre
         int ty = TQ, tx = TQ;
         if (RC.ny[i] < TQ && RC.ny[i] <= RC.nx[i]) {
             ty = RC.ny[i];
-            tx = cap / (ty + 2 * H) - 2 * H;
+            // a quarter-size region: thin strips are latency-bound, so
+            // spread them over 4x more CTAs
+            tx = max(cap / 4 / (ty + 2 * H) - 2 * H, 8);
         } else if (RC.nx[i] < TQ) {
             tx = RC.nx[i];
-            ty = cap / (tx + 2 * H) - 2 * H;
+            ty = max(cap / 4 / (tx + 2 * H) - 2 * H, 8);
         }
         R.y0[R.n] = RC.y0[i];
         R.x0[R.n] = RC.x0[i];
