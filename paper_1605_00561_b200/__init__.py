@@ -22,7 +22,7 @@ from dataclasses import dataclass
 from .schemes import BOUNDARIES, SCHEMES, WAVELETS  # noqa: F401
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libwavelift_b200.so")
+LIB_PATH = os.environ.get("WL_LIB") or os.path.join(_PKG, "libwavelift_b200.so")
 
 WL_OK, WL_EINVAL, WL_ERUNTIME = 0, 1, 2
 ENGINE_AUTO, ENGINE_INTERP, ENGINE_FAST = 0, 1, 2

@@ -14,13 +14,16 @@ from concurrent.futures import ThreadPoolExecutor
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-OBJ = os.path.join(PKG, "_obj")
-LIB = os.path.join(PKG, "libwavelift_b200.so")
+# WL_VARIANT=<tag> with WL_DEFS="-DX=1 ..." builds an A/B variant library
+# (libwavelift_b200_<tag>.so) for tuning experiments; loaded via WL_LIB.
+VARIANT = os.environ.get("WL_VARIANT", "")
+OBJ = os.path.join(PKG, "_obj" + ("_" + VARIANT if VARIANT else ""))
+LIB = os.path.join(PKG, "libwavelift_b200" + ("_" + VARIANT if VARIANT else "") + ".so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
                 "--expt-relaxed-constexpr", "-Xptxas", "-v", "-ccbin", "g++",
-                "-I" + os.path.join(ROOT, "include")]
+                "-I" + os.path.join(ROOT, "include")] + os.environ.get("WL_DEFS", "").split()
 SOURCES = ["wl_capi.cu", "wl_interp.cu", "wl_fast.cu", "wl_fast_cdf53_fwd.cu",
            "wl_fast_cdf53_inv.cu", "wl_fast_cdf97_fwd.cu", "wl_fast_cdf97_inv.cu", "wl_conv.cu"]
 

@@ -41,6 +41,13 @@
 
 namespace wlfast {
 
+// Edge exchange between compute warps: 0 = one bar.sync per epoch (default),
+// 1 = split-phase mbarrier (arrive after publishing, wait before the edge
+// rows). Both execute one barrier per epoch; kept switchable for A/B runs.
+#ifndef WL_XCH_MBAR
+#define WL_XCH_MBAR 0
+#endif
+
 constexpr int CPT = 2;   // component cells per lane per row
 constexpr int TWC = 64;  // compute-region width in cells (32 lanes x CPT)
 
@@ -83,6 +90,27 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
         " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
         "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
         : "memory");
+}
+// Producer-side wait: the TMA warp is normally far ahead of the compute
+// warps, so poll with exponential back-off instead of a tight spin that
+// steals issue slots from the compute warps sharing its scheduler.
+__device__ __forceinline__ bool mbar_test(uint64_t* b, unsigned parity) {
+    unsigned ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(smem_u32(b)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* b, unsigned parity) {
+    unsigned ns = 32;
+    while (!mbar_test(b, parity)) {
+        __nanosleep(ns);
+        ns = ns < 256 ? 2 * ns : 256;
+    }
 }
 __device__ __forceinline__ void named_sync(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
@@ -149,7 +177,7 @@ __host__ __device__ constexpr bool uses_dr(unsigned long long m, int c, int dr) 
 }
 
 template <class P, int DIR, int R, int NW>
-__global__ void __launch_bounds__((NW + 1) * 32)
+__global__ void __launch_bounds__((NW + 1) * 32, 2)
     fast_kernel(const __grid_constant__ CUtensorMap m0, const __grid_constant__ CUtensorMap m1,
                 const __grid_constant__ CUtensorMap m2, const __grid_constant__ CUtensorMap m3,
                 const FastArgs a) {
@@ -160,6 +188,7 @@ __global__ void __launch_bounds__((NW + 1) * 32)
     float* xch = stage + 2 * G::kStageFloats;
     uint64_t* full = reinterpret_cast<uint64_t*>(xch + G::kXchFloats);
     uint64_t* empty = full + 2;
+    uint64_t* xbar = full + 4;  // split-phase edge-exchange barriers, one per slot
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
@@ -167,6 +196,8 @@ __global__ void __launch_bounds__((NW + 1) * 32)
         mbar_init(&full[1], 1);
         mbar_init(&empty[0], NW * 32);
         mbar_init(&empty[1], NW * 32);
+        mbar_init(&xbar[0], NW * 32);
+        mbar_init(&xbar[1], NW * 32);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -176,7 +207,7 @@ __global__ void __launch_bounds__((NW + 1) * 32)
         if (lane == 0) {
             for (int i = 0, t = blockIdx.x; t < a.ntiles; t += gridDim.x, ++i) {
                 const int s = i & 1;
-                if (i >= 2) mbar_wait(&empty[s], ((i >> 1) - 1) & 1);
+                if (i >= 2) mbar_wait_backoff(&empty[s], ((i >> 1) - 1) & 1);
                 const int tyi = t / a.tiles_x;
                 const int ty = tyi + a.t0, tx = t - tyi * a.tiles_x + a.t0;
                 const int cx = a.X0 + tx * a.TW - H;      // first compute cell column
@@ -201,6 +232,7 @@ __global__ void __launch_bounds__((NW + 1) * 32)
     float v[R][CPT][4];
     float gu[CPT][4], gd[CPT][4];
     int xslot = 0;
+    unsigned xphase = 0;  // parity of the next phase to wait for, per slot (bit s)
 
     for (int i = 0, t = blockIdx.x; t < a.ntiles; t += gridDim.x, ++i) {
         const int s = i & 1;
@@ -287,69 +319,89 @@ __global__ void __launch_bounds__((NW + 1) * 32)
         sfor<P::kEpochs>([&](auto e_) {
             constexpr int E = decltype(e_)::value;
             constexpr unsigned long long U = P::kUse[E];
+            // Split-phase block barrier for epochs > 0: publish the edge rows
+            // and ARRIVE, compute the rows that need no neighbour-warp data,
+            // then WAIT and finish the two edge rows. Still exactly one
+            // barrier (one mbarrier phase) per epoch per tile.
+            // Layout [slot][warp][top|bottom][column c][lane] float4: every
+            // warp-wide access is a contiguous 512 B run (4 wavefronts).
+            constexpr int kRowF = CPT * 32 * 4;  // floats per published row
+            float* xw = xch + (xslot * NW + warp) * 2 * kRowF;
             if constexpr (E > 0) {
-                // Publish edge rows, one block barrier, fetch neighbours'.
-                float* x = xch + ((xslot * NW + warp) * 2) * (32 * CPT * 4);
-                float4* top = reinterpret_cast<float4*>(x + lane * CPT * 4);
-                float4* bot = reinterpret_cast<float4*>(x + 32 * CPT * 4 + lane * CPT * 4);
 #pragma unroll
                 for (int c = 0; c < CPT; ++c) {
-                    top[c] = make_float4(v[0][c][0], v[0][c][1], v[0][c][2], v[0][c][3]);
-                    bot[c] = make_float4(v[R - 1][c][0], v[R - 1][c][1], v[R - 1][c][2],
-                                         v[R - 1][c][3]);
+                    reinterpret_cast<float4*>(xw + c * 128)[lane] =
+                        make_float4(v[0][c][0], v[0][c][1], v[0][c][2], v[0][c][3]);
+                    reinterpret_cast<float4*>(xw + kRowF + c * 128)[lane] = make_float4(
+                        v[R - 1][c][0], v[R - 1][c][1], v[R - 1][c][2], v[R - 1][c][3]);
                 }
-                named_sync(1, NW * 32);
-                if (warp > 0) {
-                    const float4* nb = reinterpret_cast<const float4*>(
-                        x - 2 * 32 * CPT * 4 + 32 * CPT * 4 + lane * CPT * 4);
-#pragma unroll
-                    for (int c = 0; c < CPT; ++c) {
-                        const float4 q = nb[c];
-                        gu[c][0] = q.x; gu[c][1] = q.y; gu[c][2] = q.z; gu[c][3] = q.w;
-                    }
-                }
-                if (warp < NW - 1) {
-                    const float4* nb =
-                        reinterpret_cast<const float4*>(x + 2 * 32 * CPT * 4 + lane * CPT * 4);
-#pragma unroll
-                    for (int c = 0; c < CPT; ++c) {
-                        const float4 q = nb[c];
-                        gd[c][0] = q.x; gd[c][1] = q.y; gd[c][2] = q.z; gd[c][3] = q.w;
-                    }
-                }
-                xslot ^= 1;
+#if WL_XCH_MBAR
+                mbar_arrive(&xbar[xslot]);  // release: this lane's edge stores
+#else
+                named_sync(1, NW * 32);  // the epoch's block barrier
+#endif
             }
             // Horizontal neighbours of the lane's edge columns (warp shuffle).
             float sl[R + 2][4], sr[R + 2][4];
             sfor<4>([&](auto c_) {
                 constexpr int C = decltype(c_)::value;
                 if constexpr (uses_dc(U, C, -1)) {
-                    if constexpr (uses(U, C, -1, -1))
-                        sl[0][C] = __shfl_up_sync(0xffffffffu, gu[CPT - 1][C], 1);
 #pragma unroll
                     for (int r = 0; r < R; ++r)
                         sl[r + 1][C] = __shfl_up_sync(0xffffffffu, v[r][CPT - 1][C], 1);
-                    if constexpr (uses(U, C, 1, -1))
-                        sl[R + 1][C] = __shfl_up_sync(0xffffffffu, gd[CPT - 1][C], 1);
                 }
                 if constexpr (uses_dc(U, C, 1)) {
-                    if constexpr (uses(U, C, -1, 1))
-                        sr[0][C] = __shfl_down_sync(0xffffffffu, gu[0][C], 1);
 #pragma unroll
                     for (int r = 0; r < R; ++r)
                         sr[r + 1][C] = __shfl_down_sync(0xffffffffu, v[r][0][C], 1);
-                    if constexpr (uses(U, C, 1, 1))
-                        sr[R + 1][C] = __shfl_down_sync(0xffffffffu, gd[0][C], 1);
                 }
             });
             float o[R][CPT][4];
-            sfor<R>([&](auto r_) {
+            auto row = [&](auto r_) {
                 sfor<CPT>([&](auto c_) {
                     constexpr int RR = decltype(r_)::value, CC = decltype(c_)::value;
                     Acc<R, RR, CC> acc{v, gu, gd, sl, sr};
                     P::template nbr<E>(acc, o[RR][CC]);
                 });
+            };
+            // interior rows 1..R-2 read only this warp's rows
+            sfor<R - 2>([&](auto r_) { row(std::integral_constant<int, decltype(r_)::value + 1>{}); });
+            if constexpr (E > 0) {
+#if WL_XCH_MBAR
+                mbar_wait(&xbar[xslot], (xphase >> xslot) & 1);
+                xphase ^= 1u << xslot;
+#endif
+                if (warp > 0) {  // bottom row of the warp above
+                    const float* nb = xw - 2 * kRowF + kRowF;
+#pragma unroll
+                    for (int c = 0; c < CPT; ++c) {
+                        const float4 q = reinterpret_cast<const float4*>(nb + c * 128)[lane];
+                        gu[c][0] = q.x; gu[c][1] = q.y; gu[c][2] = q.z; gu[c][3] = q.w;
+                    }
+                }
+                if (warp < NW - 1) {  // top row of the warp below
+                    const float* nb = xw + 2 * kRowF;
+#pragma unroll
+                    for (int c = 0; c < CPT; ++c) {
+                        const float4 q = reinterpret_cast<const float4*>(nb + c * 128)[lane];
+                        gd[c][0] = q.x; gd[c][1] = q.y; gd[c][2] = q.z; gd[c][3] = q.w;
+                    }
+                }
+                xslot ^= 1;
+            }
+            sfor<4>([&](auto c_) {
+                constexpr int C = decltype(c_)::value;
+                if constexpr (uses(U, C, -1, -1))
+                    sl[0][C] = __shfl_up_sync(0xffffffffu, gu[CPT - 1][C], 1);
+                if constexpr (uses(U, C, 1, -1))
+                    sl[R + 1][C] = __shfl_up_sync(0xffffffffu, gd[CPT - 1][C], 1);
+                if constexpr (uses(U, C, -1, 1))
+                    sr[0][C] = __shfl_down_sync(0xffffffffu, gu[0][C], 1);
+                if constexpr (uses(U, C, 1, 1))
+                    sr[R + 1][C] = __shfl_down_sync(0xffffffffu, gd[0][C], 1);
             });
+            row(std::integral_constant<int, 0>{});
+            row(std::integral_constant<int, R - 1>{});
 #pragma unroll
             for (int r = 0; r < R; ++r)
 #pragma unroll
@@ -367,41 +419,53 @@ __global__ void __launch_bounds__((NW + 1) * 32)
         const bool c0 = CPT * lane >= H && CPT * lane < H + a.TW && gx >= 0 && gx < a.qw;
         const bool c1 =
             CPT * lane + 1 >= H && CPT * lane + 1 < H + a.TW && gx + 1 >= 0 && gx + 1 < a.qw;
+        // Branch-free, predicated stores: both cells (vector store) / only
+        // the left / only the right cell. Row validity is warp-uniform.
+        const bool both = c0 && c1, only0 = c0 && !c1, only1 = c1 && !c0;
+        if (DIR == 0 && a.scaling) {  // scale_planes (transform.cpp:154-159)
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+#pragma unroll
+                for (int c = 0; c < CPT; ++c) {
+                    v[r][c][0] *= a.scale;
+                    v[r][c][3] /= a.scale;
+                }
+        }
+        // 64-bit row pointers of the lane's first cell, advanced per row
+        float* pk[4];
+        const long off0 = DIR == 0 ? (long)gy0 * a.out_pitch + gx
+                                   : (long)(2 * gy0) * a.out_pitch + 2 * gx;
+#pragma unroll
+        for (int k = 0; k < (DIR == 0 ? 4 : 1); ++k) pk[k] = a.out[k] + off0;
+        const long step = DIR == 0 ? a.out_pitch : 2 * a.out_pitch;
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             const int qr = warp * R + r;
             const int gy = gy0 + r;
-            if (qr < H || qr >= H + a.TH || gy < 0 || gy >= a.qh) continue;
+            const bool row_ok = qr >= H && qr < H + a.TH && gy >= 0 && gy < a.qh;
             if (DIR == 0) {
-                float lo[4] = {v[r][0][0], v[r][0][1], v[r][0][2], v[r][0][3]};
-                float hi[4] = {v[r][1][0], v[r][1][1], v[r][1][2], v[r][1][3]};
-                if (a.scaling) {  // scale_planes (transform.cpp:154-159)
-                    lo[0] *= a.scale; lo[3] /= a.scale;
-                    hi[0] *= a.scale; hi[3] /= a.scale;
-                }
-                const long off = (long)gy * a.out_pitch + gx;
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
-                    float* p = a.out[k] + off;
-                    if (c0 && c1)
-                        *reinterpret_cast<float2*>(p) = make_float2(lo[k], hi[k]);
-                    else if (c0)
-                        p[0] = lo[k];
-                    else if (c1)
-                        p[1] = hi[k];
+                    float* p = pk[k] + r * step;
+                    if (row_ok && both)
+                        *reinterpret_cast<float2*>(p) = make_float2(v[r][0][k], v[r][1][k]);
+                    if (row_ok && only0) p[0] = v[r][0][k];
+                    if (row_ok && only1) p[1] = v[r][1][k];
                 }
             } else {
-                float* p0 = a.out[0] + (long)(2 * gy) * a.out_pitch + 2 * gx;
+                float* p0 = pk[0] + r * step;
                 float* p1 = p0 + a.out_pitch;
-                if (c0 && c1) {
+                if (row_ok && both) {
                     *reinterpret_cast<float4*>(p0) =
                         make_float4(v[r][0][0], v[r][0][1], v[r][1][0], v[r][1][1]);
                     *reinterpret_cast<float4*>(p1) =
                         make_float4(v[r][0][2], v[r][0][3], v[r][1][2], v[r][1][3]);
-                } else if (c0) {
+                }
+                if (row_ok && only0) {
                     *reinterpret_cast<float2*>(p0) = make_float2(v[r][0][0], v[r][0][1]);
                     *reinterpret_cast<float2*>(p1) = make_float2(v[r][0][2], v[r][0][3]);
-                } else if (c1) {
+                }
+                if (row_ok && only1) {
                     *reinterpret_cast<float2*>(p0 + 2) = make_float2(v[r][1][0], v[r][1][1]);
                     *reinterpret_cast<float2*>(p1 + 2) = make_float2(v[r][1][2], v[r][1][3]);
                 }
@@ -422,13 +486,28 @@ bool make_map(CUtensorMap* m, const float* base, int w, int h, long pitch, int b
 // Launch configuration per wavelet: (R, NW).
 template <int WAVELET>
 struct Config;
+// Tile geometry per wavelet, tuned on B200 at 16384^2 (fwd+inv pairs, see
+// profiles/tuning_r01.md): cdf53 R=3 x NW=8 (3 CTAs/SM, 27 warps),
+// cdf97 R=8 x NW=4 (deeper register rows, fewer exchanges per row).
+#ifndef WL_R53
+#define WL_R53 3
+#endif
+#ifndef WL_NW53
+#define WL_NW53 8
+#endif
+#ifndef WL_R97
+#define WL_R97 8
+#endif
+#ifndef WL_NW97
+#define WL_NW97 4
+#endif
 template <>
 struct Config<0> {  // cdf53, halo 1
-    static constexpr int R = 4, NW = 8;
+    static constexpr int R = WL_R53, NW = WL_NW53;
 };
 template <>
 struct Config<1> {  // cdf97, halo 2
-    static constexpr int R = 4, NW = 8;
+    static constexpr int R = WL_R97, NW = WL_NW97;
 };
 
 struct Plan {
