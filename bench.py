@@ -279,10 +279,20 @@ def run_gpu(args):
             traffic = json.load(open(tpath)).get(dom)
         except Exception:
             traffic = None
+    # FP32 side of the same kernel: MACs per quad (count_macs, schemes.cpp:176)
+    # -> FMA per pixel = MACs / 4; nominal FP32 peak 148 SMs x 128 FMA/clk x
+    # 2 FLOP x max SM clock.
+    dw, ds, dd = dom.split("/")
+    macs = schemes[(dw, ds)].info(0 if dd == "fwd" or ds == "convolution" else 1)["macs"]
+    fp32_peak = 148 * 128 * 2 * 1.965e9 / 1e12
+    fp32 = 2.0 * macs / 4.0 * n * n / (dom_t * 1e-3) / 1e12
     roofline = {"bound": "hbm", "kernel": dom, "achieved": per[dom]["hbm_gbs"], "peak": peak,
                 "peak_source": peak_src, "unit": "GB/s", "frac": per[dom]["frac"],
                 "traffic": traffic, "share_of_step": round(dom_t / step_sum, 4),
-                "algorithmic_bytes_per_launch": algo_bytes}
+                "algorithmic_bytes_per_launch": algo_bytes,
+                "fp32": {"fma_per_px": macs / 4.0, "achieved_tflops": round(fp32, 2),
+                         "peak_tflops_nominal": round(fp32_peak, 1),
+                         "frac": round(fp32 / fp32_peak, 4)}}
 
     # ---- C3 headline: cdf97 monolithic_star, 16384^2 (configs[2])
     c3 = None
