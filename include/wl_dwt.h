@@ -87,6 +87,84 @@ int wl_dwt2_pyramid_inverse(const float* pyramid, int w, int h, int levels, int 
                             int scheme, int boundary, int undo_scaling, float* img,
                             float* scratch, void* stream);
 
+/* ---------------------------------------------------------------- batches
+ * BASELINE configs[4] (independent images). The reference transforms one
+ * Image per call (transform.cpp:163, :198); these run the same per-image
+ * transform over n images in ONE launch per level (3-D TMA boxes). Image b
+ * lives at img + b*img_stride; its planes at ll/hl/lh/hh + b*plane_stride.
+ * Results are identical to n single-image calls. */
+int wl_dwt2_forward_batch(const float* img, int w, int h, long img_pitch, long img_stride,
+                          int n, int wavelet, int scheme, int boundary, int scaling, float* ll,
+                          float* hl, float* lh, float* hh, long plane_pitch, long plane_stride,
+                          void* stream);
+int wl_dwt2_inverse_batch(const float* ll, const float* hl, const float* lh, const float* hh,
+                          int qw, int qh, long plane_pitch, long plane_stride, int n, int wavelet,
+                          int scheme, int boundary, int undo_scaling, float* img, long img_pitch,
+                          long img_stride, void* stream);
+/* Batched multi_level_forward / multi_level_inverse (transform.cpp:198-256
+ * per image): images dense (pitch w) at img_stride apart, flat pyramids
+ * (wl_dwt2_pyramid_forward layout) at pyr_stride apart; `scratch` holds
+ * wl_pyramid_batch_scratch_elems(w, h, levels, n) floats. */
+size_t wl_pyramid_batch_scratch_elems(int w, int h, int levels, int n);
+int wl_dwt2_pyramid_forward_batch(const float* imgs, int w, int h, long img_stride, int n,
+                                  int levels, int wavelet, int scheme, int boundary, int scaling,
+                                  float* pyramids, long pyr_stride, float* scratch, void* stream);
+int wl_dwt2_pyramid_inverse_batch(const float* pyramids, int w, int h, long pyr_stride, int n,
+                                  int levels, int wavelet, int scheme, int boundary,
+                                  int undo_scaling, float* imgs, long img_stride, float* scratch,
+                                  void* stream);
+
+/* ------------------------------------------------------------- row strips
+ * BASELINE configs[3]: one image split into row strips (one per GPU). A strip
+ * transform computes the rows of `forward` / `inverse` (periodic boundary)
+ * that belong to the strip, bit-identical to the whole-image call, given
+ * `halo` rows of the neighbouring strips physically present above and below
+ * the strip in its buffer. cdf53/cdf97 only (the fast engine / convolution
+ * kernel); 16-byte aligned buffers and pitches.
+ * wl_strip_halo_rows: minimum halo -- pixel rows (direction 0) or plane rows
+ * (direction 1); -1 for an unsupported wavelet. */
+int wl_strip_halo_rows(int wavelet, int scheme, int direction);
+/* strip: first interior row; rows [-halo_rows, rows + halo_rows) readable.
+ * Output planes: rows/2 rows of (w/2). */
+int wl_dwt2_forward_strip(const float* strip, int w, int rows, int halo_rows, long pitch,
+                          int wavelet, int scheme, int scaling, float* ll, float* hl, float* lh,
+                          float* hh, long plane_pitch, void* stream);
+/* planes: first interior plane row; rows [-halo_qrows, qrows + halo_qrows)
+ * readable. Output: 2*qrows image rows of 2*qw pixels. */
+int wl_dwt2_inverse_strip(const float* ll, const float* hl, const float* lh, const float* hh,
+                          int qw, int qrows, int halo_qrows, long plane_pitch, int wavelet,
+                          int scheme, int undo_scaling, float* img, long img_pitch,
+                          void* stream);
+
+/* Row-strip multi-level pyramid across ranks (one process per GPU):
+ * replaces multi_level_forward (transform.cpp:198-227) for one image whose
+ * rows are split evenly over `nranks` ranks (rank r owns image rows
+ * [r*h/nranks, (r+1)*h/nranks)), periodic boundary. Every level exchanges
+ * `wl_strip_halo_rows` rows with the two neighbour strips by peer-memory
+ * stores into their buffers (CUDA IPC over NVLink) and device-side flags; no
+ * host synchronisation or collective library in the level loop.
+ *   create -> export (IPC blob, wl_strips_blob_bytes() bytes) -> exchange
+ *   blobs out of band -> connect(up = rank-1, down = rank+1, ring) -> fill
+ *   wl_strips_input (rows x w, pitch w) -> forward (stream-ordered; every
+ *   rank calls it the same number of times) -> check after a sync.
+ * The rank's pyramid slice: for each level l, its rows of HL, LH, HH
+ * ((rows>>(l+1)) x (w>>(l+1)) each), then its rows of the coarsest LL;
+ * wl_strips_slice_elems() floats. Stitching the ranks' slices plane by plane
+ * gives exactly wl_dwt2_pyramid_forward's output. */
+typedef struct WlStrips WlStrips;
+const char* wl_strips_last_error(void);
+size_t wl_strips_blob_bytes(void);
+int wl_strips_create(int w, int h, int rank, int nranks, int levels, int wavelet, int scheme,
+                     int scaling, WlStrips** out);
+int wl_strips_export(WlStrips* s, void* blob);
+int wl_strips_connect(WlStrips* s, const void* up_blob, const void* down_blob);
+float* wl_strips_input(WlStrips* s);
+size_t wl_strips_slice_elems(const WlStrips* s);
+int wl_strips_forward(WlStrips* s, float* slice, void* stream);
+/* WL_ERUNTIME if a halo wait timed out (call after synchronising). */
+int wl_strips_check(WlStrips* s);
+int wl_strips_destroy(WlStrips* s);
+
 /* Engine selection for tests/benchmarks: 0 = auto (fast register-tile engine
  * where available, generic tile interpreter otherwise), 1 = force the generic
  * interpreter, 2 = force the fast engine (WL_EINVAL where unsupported).

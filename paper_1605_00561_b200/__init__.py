@@ -52,6 +52,31 @@ def lib() -> ctypes.CDLL:
         l.wl_pyramid_scratch_elems.argtypes = [i, i, i]
         l.wl_dwt2_pyramid_forward.argtypes = [fp, i, i, i, i, i, i, i, fp, fp, vp]
         l.wl_dwt2_pyramid_inverse.argtypes = [fp, i, i, i, i, i, i, i, fp, fp, vp]
+        l.wl_dwt2_forward_batch.argtypes = [fp, i, i, lg, lg, i, i, i, i, i, fp, fp, fp, fp,
+                                            lg, lg, vp]
+        l.wl_dwt2_inverse_batch.argtypes = [fp, fp, fp, fp, i, i, lg, lg, i, i, i, i, i, fp,
+                                            lg, lg, vp]
+        l.wl_pyramid_batch_scratch_elems.restype = ctypes.c_size_t
+        l.wl_pyramid_batch_scratch_elems.argtypes = [i, i, i, i]
+        l.wl_dwt2_pyramid_forward_batch.argtypes = [fp, i, i, lg, i, i, i, i, i, i, fp, lg, fp,
+                                                    vp]
+        l.wl_dwt2_pyramid_inverse_batch.argtypes = [fp, i, i, lg, i, i, i, i, i, i, fp, lg, fp,
+                                                    vp]
+        l.wl_strip_halo_rows.argtypes = [i, i, i]
+        l.wl_dwt2_forward_strip.argtypes = [fp, i, i, i, lg, i, i, i, fp, fp, fp, fp, lg, vp]
+        l.wl_dwt2_inverse_strip.argtypes = [fp, fp, fp, fp, i, i, i, lg, i, i, i, fp, lg, vp]
+        l.wl_strips_last_error.restype = ctypes.c_char_p
+        l.wl_strips_blob_bytes.restype = ctypes.c_size_t
+        l.wl_strips_create.argtypes = [i, i, i, i, i, i, i, i, ctypes.POINTER(vp)]
+        l.wl_strips_export.argtypes = [vp, ctypes.c_char_p]
+        l.wl_strips_connect.argtypes = [vp, ctypes.c_char_p, ctypes.c_char_p]
+        l.wl_strips_input.restype = vp
+        l.wl_strips_input.argtypes = [vp]
+        l.wl_strips_slice_elems.restype = ctypes.c_size_t
+        l.wl_strips_slice_elems.argtypes = [vp]
+        l.wl_strips_forward.argtypes = [vp, fp, vp]
+        l.wl_strips_check.argtypes = [vp]
+        l.wl_strips_destroy.argtypes = [vp]
         l.wl_set_engine.argtypes = [i]
         l.wl_launch_count.restype = lg
         _lib = l
@@ -280,3 +305,265 @@ def multi_level_inverse(pyr: Pyramid, wavelet, boundary="periodic", undo_scaling
                                          int(bool(undo_scaling)), out.data_ptr(),
                                          scratch.data_ptr(), _stream_ptr(stream)))
     return out
+
+
+# ------------------------------------------------------------ batches (C5)
+def _kind(scheme):
+    if scheme is None:
+        return 0
+    return scheme.kind if isinstance(scheme, Scheme) else _index(SCHEMES, scheme, "scheme")
+
+
+def forward_batch(imgs, scheme: Scheme, boundary="periodic", apply_scaling=False, out=None,
+                  stream=None):
+    """`forward` over a batch: (n, h, w) -> (n, 4, h/2, w/2), one launch."""
+    import torch
+    imgs = _dev_f32(imgs, "imgs").contiguous()
+    if imgs.dim() != 3:
+        raise ValueError("imgs must be (n, height, width)")
+    n, h, w = imgs.shape
+    if out is None:
+        out = torch.empty((n, 4, max(h // 2, 0), max(w // 2, 0)), device=imgs.device,
+                          dtype=torch.float32)
+    b = _index(BOUNDARIES, boundary, "boundary")
+    _check(lib().wl_dwt2_forward_batch(
+        imgs.data_ptr(), w, h, w, h * w, n, scheme.wavelet.index, scheme.kind, b,
+        int(bool(apply_scaling)), out[:, 0].data_ptr(), out[:, 1].data_ptr(),
+        out[:, 2].data_ptr(), out[:, 3].data_ptr(), out.stride(2), out.stride(0),
+        _stream_ptr(stream)))
+    return out
+
+
+def inverse_batch(q, wavelet, boundary="periodic", undo_scaling=False, scheme=None, out=None,
+                  stream=None):
+    """`inverse` over a batch: (n, 4, qh, qw) -> (n, 2qh, 2qw), one launch."""
+    import torch
+    q = _dev_f32(q, "q").contiguous()
+    if q.dim() != 4 or q.shape[1] != 4:
+        raise ValueError("q must be (n, 4, qh, qw)")
+    w = wavelet if isinstance(wavelet, WaveletSpec) else get_wavelet(wavelet)
+    n, _, qh, qw = q.shape
+    if out is None:
+        out = torch.empty((n, 2 * qh, 2 * qw), device=q.device, dtype=torch.float32)
+    b = _index(BOUNDARIES, boundary, "boundary")
+    _check(lib().wl_dwt2_inverse_batch(
+        q[:, 0].data_ptr(), q[:, 1].data_ptr(), q[:, 2].data_ptr(), q[:, 3].data_ptr(), qw, qh,
+        qw, q.stride(0), n, w.index, _kind(scheme), b, int(bool(undo_scaling)), out.data_ptr(),
+        2 * qw, out.stride(0), _stream_ptr(stream)))
+    return out
+
+
+def multi_level_forward_batch(imgs, scheme: Scheme, levels: int, boundary="periodic",
+                              apply_scaling=False, out=None, scratch=None, stream=None):
+    """`multi_level_forward` over a batch (n, h, w): returns (n, h*w) flat
+    pyramids (Pyramid layout per row); one launch per level."""
+    import torch
+    imgs = _dev_f32(imgs, "imgs").contiguous()
+    if imgs.dim() != 3:
+        raise ValueError("imgs must be (n, height, width)")
+    n, h, w = imgs.shape
+    if out is None:
+        out = torch.empty((n, h * w), device=imgs.device, dtype=torch.float32)
+    need = lib().wl_pyramid_batch_scratch_elems(w, h, levels, n)
+    if scratch is None or scratch.numel() < need:
+        scratch = torch.empty(max(need, 1), device=imgs.device, dtype=torch.float32)
+    _check(lib().wl_dwt2_pyramid_forward_batch(
+        imgs.data_ptr(), w, h, h * w, n, levels, scheme.wavelet.index, scheme.kind,
+        _index(BOUNDARIES, boundary, "boundary"), int(bool(apply_scaling)), out.data_ptr(),
+        out.stride(0), scratch.data_ptr(), _stream_ptr(stream)))
+    return out
+
+
+def multi_level_inverse_batch(pyrs, width, height, levels, wavelet, boundary="periodic",
+                              undo_scaling=False, scheme=None, out=None, scratch=None,
+                              stream=None):
+    """`multi_level_inverse` over a batch of flat pyramids (n, h*w)."""
+    import torch
+    pyrs = _dev_f32(pyrs, "pyramids").contiguous()
+    n = pyrs.shape[0]
+    if pyrs.dim() != 2 or pyrs.shape[1] != width * height:
+        raise ValueError("pyramid detail plane size does not match its level")
+    w = wavelet if isinstance(wavelet, WaveletSpec) else get_wavelet(wavelet)
+    if out is None:
+        out = torch.empty((n, height, width), device=pyrs.device, dtype=torch.float32)
+    need = lib().wl_pyramid_batch_scratch_elems(width, height, levels, n)
+    if scratch is None or scratch.numel() < need:
+        scratch = torch.empty(max(need, 1), device=pyrs.device, dtype=torch.float32)
+    _check(lib().wl_dwt2_pyramid_inverse_batch(
+        pyrs.data_ptr(), width, height, pyrs.stride(0), n, levels, w.index, _kind(scheme),
+        _index(BOUNDARIES, boundary, "boundary"), int(bool(undo_scaling)), out.data_ptr(),
+        out.stride(0), scratch.data_ptr(), _stream_ptr(stream)))
+    return out
+
+
+# ------------------------------------------------------- row strips (C4)
+def strip_halo_rows(wavelet, scheme="monolithic_star", direction=0) -> int:
+    """Halo (pixel rows for the forward, plane rows for the inverse) a strip
+    transform needs on each side."""
+    w = wavelet if isinstance(wavelet, WaveletSpec) else get_wavelet(wavelet)
+    r = lib().wl_strip_halo_rows(w.index, _kind(scheme), direction)
+    if r < 0:
+        raise ValueError("strip transforms support cdf53/cdf97")
+    return r
+
+
+def forward_strip(buf, halo_rows: int, scheme: Scheme, apply_scaling=False, out=None,
+                  stream=None):
+    """Forward transform of the interior rows of a row strip.
+
+    `buf` is (halo + rows + halo, w): the strip's own rows plus `halo_rows`
+    rows of the neighbouring strips above and below (periodic image). The
+    result (4, rows/2, w/2) equals the matching rows of `forward` of the whole
+    image, bit for bit."""
+    import torch
+    buf = _dev_f32(buf, "buf")
+    if buf.dim() != 2 or buf.stride(1) != 1:
+        raise ValueError("buf must be a row-major 2-D tensor")
+    rows = buf.shape[0] - 2 * halo_rows
+    w = buf.shape[1]
+    if out is None:
+        out = torch.empty((4, max(rows // 2, 0), w // 2), device=buf.device, dtype=torch.float32)
+    interior = buf[halo_rows:]
+    _check(lib().wl_dwt2_forward_strip(
+        interior.data_ptr(), w, rows, halo_rows, buf.stride(0), scheme.wavelet.index, scheme.kind,
+        int(bool(apply_scaling)), out[0].data_ptr(), out[1].data_ptr(), out[2].data_ptr(),
+        out[3].data_ptr(), out.stride(1), _stream_ptr(stream)))
+    return out
+
+
+def inverse_strip(q, halo_rows: int, wavelet, undo_scaling=False, scheme=None, out=None,
+                  stream=None):
+    """Inverse of a strip of planes `q` (4, halo + qrows + halo, qw) -> image
+    rows (2*qrows, 2*qw)."""
+    import torch
+    q = _dev_f32(q, "q").contiguous()
+    if q.dim() != 3 or q.shape[0] != 4:
+        raise ValueError("q must be (4, rows, qw)")
+    w = wavelet if isinstance(wavelet, WaveletSpec) else get_wavelet(wavelet)
+    qrows = q.shape[1] - 2 * halo_rows
+    qw = q.shape[2]
+    if out is None:
+        out = torch.empty((2 * max(qrows, 0), 2 * qw), device=q.device, dtype=torch.float32)
+    p = [q[c, halo_rows:].data_ptr() for c in range(4)]
+    _check(lib().wl_dwt2_inverse_strip(p[0], p[1], p[2], p[3], qw, qrows, halo_rows, qw,
+                                       w.index, _kind(scheme), int(bool(undo_scaling)),
+                                       out.data_ptr(), out.stride(0), _stream_ptr(stream)))
+    return out
+
+
+class _DevView:
+    """__cuda_array_interface__ over a raw device pointer (zero-copy view)."""
+
+    def __init__(self, ptr, shape):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": "<f4",
+                                         "data": (int(ptr), False), "version": 3,
+                                         "strides": None}
+
+
+def _scheck(status: int):
+    if status == WL_OK:
+        return
+    msg = lib().wl_strips_last_error().decode()
+    raise (ValueError if status == WL_EINVAL else RuntimeError)(msg)
+
+
+class StripPyramid:
+    """One rank's share of a row-strip multi-level pyramid (configs[3]).
+
+    Rank `rank` of `nranks` owns image rows [rank*h/nranks, (rank+1)*h/nranks)
+    of an h x w image (periodic boundary). Levels exchange halo rows with the
+    neighbour ranks through peer memory (CUDA IPC), see include/wl_dwt.h.
+    Usage: `export()` -> share blobs -> `connect(up, down)` -> write
+    `input` -> `forward()` (collective: every rank calls it equally often)."""
+
+    def __init__(self, w, h, levels, scheme: Scheme, rank=0, nranks=1, apply_scaling=False):
+        self.w, self.h, self.levels = w, h, levels
+        self.rank, self.nranks = rank, nranks
+        self.rows = h // nranks if nranks > 0 else 0
+        self.scheme = scheme
+        self._ctx = ctypes.c_void_p()
+        _scheck(lib().wl_strips_create(w, h, rank, nranks, levels, scheme.wavelet.index,
+                                       scheme.kind, int(bool(apply_scaling)),
+                                       ctypes.byref(self._ctx)))
+        import torch
+        self.input = torch.as_tensor(_DevView(lib().wl_strips_input(self._ctx),
+                                              (self.rows, w)), device="cuda")
+        if nranks == 1:
+            b = self.export()
+            self.connect(b, b)
+
+    def export(self) -> bytes:
+        buf = ctypes.create_string_buffer(lib().wl_strips_blob_bytes())
+        _scheck(lib().wl_strips_export(self._ctx, buf))
+        return buf.raw
+
+    def connect(self, up: bytes, down: bytes):
+        _scheck(lib().wl_strips_connect(self._ctx, up, down))
+
+    def slice_elems(self) -> int:
+        return lib().wl_strips_slice_elems(self._ctx)
+
+    def forward(self, out=None, stream=None):
+        import torch
+        if out is None:
+            out = torch.empty(self.slice_elems(), device="cuda", dtype=torch.float32)
+        _scheck(lib().wl_strips_forward(self._ctx, out.data_ptr(), _stream_ptr(stream)))
+        return out
+
+    def check(self):
+        _scheck(lib().wl_strips_check(self._ctx))
+
+    def close(self):
+        if self._ctx:
+            lib().wl_strips_destroy(self._ctx)
+            self._ctx = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def strip_slice_planes(slice_, w, rows, levels):
+    """Views of a rank's pyramid slice: [(hl, lh, hh) per level], ll."""
+    out, off = [], 0
+    for l in range(levels):
+        qw, qr = w >> (l + 1), rows >> (l + 1)
+        n = qw * qr
+        out.append(tuple(slice_[off + i * n: off + (i + 1) * n].view(qr, qw) for i in range(3)))
+        off += 3 * n
+    qw, qr = w >> levels, rows >> levels
+    return out, slice_[off: off + qw * qr].view(qr, qw)
+
+
+def stitch_strip_pyramid(slices, w, h, levels):
+    """Concatenates the ranks' slices (rank order) into the flat
+    multi_level_forward layout (Pyramid.flat)."""
+    import torch
+    n = len(slices)
+    rows = h // n
+    parts = [strip_slice_planes(s, w, rows, levels) for s in slices]
+    flat = []
+    for l in range(levels):
+        for i in range(3):
+            flat.append(torch.cat([p[0][l][i] for p in parts], 0).reshape(-1))
+    flat.append(torch.cat([p[1] for p in parts], 0).reshape(-1))
+    return torch.cat(flat)
+
+
+def strip_pyramid_distributed(img_rows, w, h, levels, scheme: Scheme, group=None,
+                              apply_scaling=False):
+    """Builds and connects this rank's StripPyramid over torch.distributed
+    (blobs exchanged with all_gather_object; ring neighbours) and fills its
+    input with `img_rows` (rows x w on this rank's GPU)."""
+    import torch.distributed as dist
+    rank, n = dist.get_rank(group), dist.get_world_size(group)
+    sp = StripPyramid(w, h, levels, scheme, rank, n, apply_scaling)
+    if n > 1:
+        blobs = [None] * n
+        dist.all_gather_object(blobs, sp.export(), group=group)
+        sp.connect(blobs[(rank - 1) % n], blobs[(rank + 1) % n])
+    if img_rows is not None:
+        sp.input.copy_(img_rows)
+    return sp

@@ -57,6 +57,43 @@ int launch_level(WlLevel L, cudaStream_t s) {
     return cuda_status(e, "interp_kernel");
 }
 
+// Batched launch: the fast engine / conv kernel take the batch in one launch
+// (3-D TMA maps); every other engine loops over the images.
+int launch_level_batch(WlLevel L, cudaStream_t s) {
+    if (L.nb <= 1) {
+        L.nb = 1;
+        return launch_level(L, s);
+    }
+    WlLevel Lp = L;
+    if (Lp.direction == 1 && Lp.scheme == WL_CONVOLUTION) {
+        Lp.scheme = WL_SWELDENS;
+        Lp.prog = prog_index(Lp.wavelet, Lp.scheme, 1);
+    }
+    const WlProgram& P = wl_host_program(Lp.prog);
+    const int engine = g_engine.load();
+    const bool batched = engine != 1 && Lp.wavelet <= 1 &&
+                         (P.is_conv ? (L.in_bstride[0] % 4 == 0) : wl_fast_supported(Lp));
+    if (batched) return launch_level(L, s);
+    for (int b = 0; b < L.nb; ++b) {
+        WlLevel Li = L;
+        Li.nb = 1;
+        for (int k = 0; k < 4; ++k) {
+            if (Li.in[k]) Li.in[k] += b * L.in_bstride[k];
+            if (Li.out[k]) Li.out[k] += b * L.out_bstride[k];
+        }
+        const int st = launch_level(Li, s);
+        if (st != WL_OK) return st;
+    }
+    return WL_OK;
+}
+
+// Strip halo in pixel rows (forward) / plane rows (inverse) the fast engine
+// needs around a window: the program's reach plus the tiles' ghost row.
+int strip_halo(int wavelet, int direction) {
+    const int H = wavelet == WL_CDF53 ? 1 : 2;  // required_halo (parsim.cpp:185-218)
+    return direction == 0 ? 2 * (H + 1) : H + 1;
+}
+
 }  // namespace
 
 void wl_count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
@@ -157,6 +194,156 @@ int wl_dwt2_inverse(const float* ll, const float* hl, const float* lh, const flo
     return launch_level(L, static_cast<cudaStream_t>(stream));
 }
 
+int wl_dwt2_forward_batch(const float* img, int w, int h, long img_pitch, long img_stride,
+                          int n, int wavelet, int scheme, int boundary, int scaling, float* ll,
+                          float* hl, float* lh, float* hh, long plane_pitch, long plane_stride,
+                          void* stream) {
+    if (n < 0) return fail(WL_EINVAL, "batch size must be >= 0");
+    if (n == 0) return WL_OK;
+    if (w <= 0 || h <= 0 || w % 2 != 0 || h % 2 != 0)
+        return fail(WL_EINVAL, "forward requires even positive dimensions");
+    if (!valid_ids(wavelet, scheme, boundary))
+        return fail(WL_EINVAL, "unknown wavelet/scheme/boundary");
+    if (!img || !ll || !hl || !lh || !hh) return fail(WL_EINVAL, "null buffer");
+    if (img_pitch < w || plane_pitch < w / 2) return fail(WL_EINVAL, "pitch too small");
+    if (n > 1 && (img_stride < img_pitch * h || plane_stride < plane_pitch * (h / 2)))
+        return fail(WL_EINVAL, "batch stride too small");
+    WlLevel L{};
+    L.in[0] = img;
+    L.out[0] = ll;
+    L.out[1] = hl;
+    L.out[2] = lh;
+    L.out[3] = hh;
+    L.qw = w / 2;
+    L.qh = h / 2;
+    L.in_pitch = img_pitch;
+    L.out_pitch = plane_pitch;
+    L.wavelet = wavelet;
+    L.scheme = scheme;
+    L.direction = 0;
+    L.prog = prog_index(wavelet, scheme, 0);
+    L.boundary = boundary;
+    L.scaling = scaling != 0;
+    L.nb = n;
+    L.in_bstride[0] = img_stride;
+    for (int k = 0; k < 4; ++k) L.out_bstride[k] = plane_stride;
+    return launch_level_batch(L, static_cast<cudaStream_t>(stream));
+}
+
+int wl_dwt2_inverse_batch(const float* ll, const float* hl, const float* lh, const float* hh,
+                          int qw, int qh, long plane_pitch, long plane_stride, int n, int wavelet,
+                          int scheme, int boundary, int undo_scaling, float* img, long img_pitch,
+                          long img_stride, void* stream) {
+    if (n < 0) return fail(WL_EINVAL, "batch size must be >= 0");
+    if (n == 0) return WL_OK;
+    if (qw <= 0 || qh <= 0) return fail(WL_EINVAL, "inverse requires positive plane dimensions");
+    if (!valid_ids(wavelet, scheme, boundary))
+        return fail(WL_EINVAL, "unknown wavelet/scheme/boundary");
+    if (!img || !ll || !hl || !lh || !hh) return fail(WL_EINVAL, "null buffer");
+    if (img_pitch < 2 * qw || plane_pitch < qw) return fail(WL_EINVAL, "pitch too small");
+    if (n > 1 && (img_stride < img_pitch * 2 * qh || plane_stride < plane_pitch * qh))
+        return fail(WL_EINVAL, "batch stride too small");
+    WlLevel L{};
+    L.in[0] = ll;
+    L.in[1] = hl;
+    L.in[2] = lh;
+    L.in[3] = hh;
+    L.out[0] = img;
+    L.qw = qw;
+    L.qh = qh;
+    L.in_pitch = plane_pitch;
+    L.out_pitch = img_pitch;
+    L.wavelet = wavelet;
+    L.scheme = scheme;
+    L.direction = 1;
+    L.prog = prog_index(wavelet, scheme, 1);
+    L.boundary = boundary;
+    L.scaling = undo_scaling != 0;
+    L.nb = n;
+    for (int k = 0; k < 4; ++k) L.in_bstride[k] = plane_stride;
+    L.out_bstride[0] = img_stride;
+    return launch_level_batch(L, static_cast<cudaStream_t>(stream));
+}
+
+int wl_strip_halo_rows(int wavelet, int scheme, int direction) {
+    if (!valid_ids(wavelet, scheme, 0) || wavelet > WL_CDF97 || direction < 0 || direction > 1)
+        return -1;
+    return strip_halo(wavelet, direction);
+}
+
+int wl_dwt2_forward_strip(const float* strip, int w, int rows, int halo_rows, long pitch,
+                          int wavelet, int scheme, int scaling, float* ll, float* hl, float* lh,
+                          float* hh, long plane_pitch, void* stream) {
+    if (w <= 0 || rows <= 0 || w % 2 != 0 || rows % 2 != 0)
+        return fail(WL_EINVAL, "forward requires even positive dimensions");
+    if (!valid_ids(wavelet, scheme, 0) || wavelet > WL_CDF97)
+        return fail(WL_EINVAL, "strip transforms support cdf53/cdf97");
+    if (halo_rows % 2 != 0 || halo_rows < strip_halo(wavelet, 0))
+        return fail(WL_EINVAL, "strip halo too small (see wl_strip_halo_rows) or odd");
+    if (!strip || !ll || !hl || !lh || !hh) return fail(WL_EINVAL, "null buffer");
+    if (pitch < w || plane_pitch < w / 2) return fail(WL_EINVAL, "pitch too small");
+    WlLevel L{};
+    L.in[0] = strip - static_cast<long>(halo_rows) * pitch;
+    L.out[0] = ll;
+    L.out[1] = hl;
+    L.out[2] = lh;
+    L.out[3] = hh;
+    L.qw = w / 2;
+    L.qh = rows / 2 + halo_rows;
+    L.in_pitch = pitch;
+    L.out_pitch = plane_pitch;
+    L.wavelet = wavelet;
+    L.scheme = scheme;
+    L.direction = 0;
+    L.prog = prog_index(wavelet, scheme, 0);
+    L.boundary = WL_PERIODIC;
+    L.scaling = scaling != 0;
+    L.ylo = halo_rows / 2;
+    L.yhi = L.ylo + rows / 2;
+    const WlProgram& P = wl_host_program(L.prog);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (P.is_conv) return cuda_status(wl_launch_conv_fast(L, s), "conv_kernel");
+    if (!wl_fast_supported(L))
+        return fail(WL_EINVAL, "strip transform needs 16-byte aligned buffers and pitches");
+    return cuda_status(wl_launch_fast(L, s), "fast_kernel");
+}
+
+int wl_dwt2_inverse_strip(const float* ll, const float* hl, const float* lh, const float* hh,
+                          int qw, int qrows, int halo_qrows, long plane_pitch, int wavelet,
+                          int scheme, int undo_scaling, float* img, long img_pitch,
+                          void* stream) {
+    if (qw <= 0 || qrows <= 0) return fail(WL_EINVAL, "inverse requires positive plane dimensions");
+    if (!valid_ids(wavelet, scheme, 0) || wavelet > WL_CDF97)
+        return fail(WL_EINVAL, "strip transforms support cdf53/cdf97");
+    if (halo_qrows < strip_halo(wavelet, 1))
+        return fail(WL_EINVAL, "strip halo too small (see wl_strip_halo_rows)");
+    if (!img || !ll || !hl || !lh || !hh) return fail(WL_EINVAL, "null buffer");
+    if (img_pitch < 2 * qw || plane_pitch < qw) return fail(WL_EINVAL, "pitch too small");
+    if (scheme == WL_CONVOLUTION) scheme = WL_SWELDENS;
+    const long back = static_cast<long>(halo_qrows) * plane_pitch;
+    WlLevel L{};
+    L.in[0] = ll - back;
+    L.in[1] = hl - back;
+    L.in[2] = lh - back;
+    L.in[3] = hh - back;
+    L.out[0] = img;
+    L.qw = qw;
+    L.qh = qrows + 2 * halo_qrows;
+    L.in_pitch = plane_pitch;
+    L.out_pitch = img_pitch;
+    L.wavelet = wavelet;
+    L.scheme = scheme;
+    L.direction = 1;
+    L.prog = prog_index(wavelet, scheme, 1);
+    L.boundary = WL_PERIODIC;
+    L.scaling = undo_scaling != 0;
+    L.ylo = halo_qrows;
+    L.yhi = halo_qrows + qrows;
+    if (!wl_fast_supported(L))
+        return fail(WL_EINVAL, "strip transform needs 16-byte aligned buffers and pitches");
+    return cuda_status(wl_launch_fast(L, static_cast<cudaStream_t>(stream)), "fast_kernel");
+}
+
 size_t wl_pyramid_elems(int w, int h, int levels) {
     if (w <= 0 || h <= 0 || levels < 1) return 0;
     return static_cast<size_t>(w) * static_cast<size_t>(h);  // sum of 3n_l + n_L = w*h
@@ -228,6 +415,130 @@ int wl_dwt2_pyramid_inverse(const float* pyramid, int w, int h, int levels, int 
                                        boundary, undo_scaling, out, 2 * qw, stream);
         if (st != WL_OK) return st;
         ll = out;
+    }
+    return WL_OK;
+}
+
+size_t wl_pyramid_batch_scratch_elems(int w, int h, int levels, int n) {
+    if (w <= 0 || h <= 0 || levels < 1 || n < 1) return 0;
+    const size_t q1 = static_cast<size_t>(w / 2) * (h / 2);
+    return static_cast<size_t>(n) * (q1 + (levels > 1 ? q1 / 4 : 0));
+}
+
+// Batched multi_level_forward (transform.cpp:198-227 per image): one launch
+// per level for the whole batch. Image b is at imgs + b*img_stride (pitch w),
+// its flat pyramid at pyramids + b*pyr_stride; level LL planes ping-pong in
+// `scratch` (wl_pyramid_batch_scratch_elems floats).
+int wl_dwt2_pyramid_forward_batch(const float* imgs, int w, int h, long img_stride, int n,
+                                  int levels, int wavelet, int scheme, int boundary, int scaling,
+                                  float* pyramids, long pyr_stride, float* scratch,
+                                  void* stream) {
+    if (n < 0) return fail(WL_EINVAL, "batch size must be >= 0");
+    if (levels < 1) return fail(WL_EINVAL, "levels must be >= 1");
+    if (w <= 0 || h <= 0) return fail(WL_EINVAL, "forward requires even positive dimensions");
+    if (levels > 30 || w % (1 << levels) != 0 || h % (1 << levels) != 0)
+        return fail(WL_EINVAL, "image dimensions must be divisible by 2^levels");
+    if (!valid_ids(wavelet, scheme, boundary))
+        return fail(WL_EINVAL, "unknown wavelet/scheme/boundary");
+    if (n == 0) return WL_OK;
+    if (!imgs || !pyramids || !scratch) return fail(WL_EINVAL, "null buffer");
+    if (n > 1 && (img_stride < static_cast<long>(w) * h || pyr_stride < static_cast<long>(w) * h))
+        return fail(WL_EINVAL, "batch stride too small");
+    const size_t q1 = static_cast<size_t>(w / 2) * (h / 2);
+    float* ping[2] = {scratch, scratch + static_cast<size_t>(n) * q1};
+    const float* src = imgs;
+    long src_stride = img_stride;
+    size_t off = 0;
+    int cw = w, ch = h;
+    for (int l = 0; l < levels; ++l) {
+        const int qw = cw / 2, qh = ch / 2;
+        const long np = static_cast<long>(qw) * qh;
+        float* hl = pyramids + off;
+        off += 3 * np;
+        const bool last = l + 1 == levels;
+        WlLevel L{};
+        L.in[0] = src;
+        L.out[0] = last ? pyramids + off : ping[l & 1];
+        L.out[1] = hl;
+        L.out[2] = hl + np;
+        L.out[3] = hl + 2 * np;
+        L.qw = qw;
+        L.qh = qh;
+        L.in_pitch = cw;
+        L.out_pitch = qw;
+        L.wavelet = wavelet;
+        L.scheme = scheme;
+        L.direction = 0;
+        L.prog = prog_index(wavelet, scheme, 0);
+        L.boundary = boundary;
+        L.scaling = scaling != 0;
+        L.nb = n;
+        L.in_bstride[0] = src_stride;
+        L.out_bstride[0] = last ? pyr_stride : np;
+        L.out_bstride[1] = L.out_bstride[2] = L.out_bstride[3] = pyr_stride;
+        const int st = launch_level_batch(L, static_cast<cudaStream_t>(stream));
+        if (st != WL_OK) return st;
+        src = L.out[0];
+        src_stride = L.out_bstride[0];
+        cw = qw;
+        ch = qh;
+    }
+    return WL_OK;
+}
+
+// Batched multi_level_inverse (transform.cpp:229-256 per image).
+int wl_dwt2_pyramid_inverse_batch(const float* pyramids, int w, int h, long pyr_stride, int n,
+                                  int levels, int wavelet, int scheme, int boundary,
+                                  int undo_scaling, float* imgs, long img_stride, float* scratch,
+                                  void* stream) {
+    if (n < 0) return fail(WL_EINVAL, "batch size must be >= 0");
+    if (levels < 1) return fail(WL_EINVAL, "levels must be >= 1");
+    if (w <= 0 || h <= 0 || levels > 30 || w % (1 << levels) != 0 || h % (1 << levels) != 0)
+        return fail(WL_EINVAL, "pyramid level dimensions are inconsistent");
+    if (!valid_ids(wavelet, scheme, boundary))
+        return fail(WL_EINVAL, "unknown wavelet/scheme/boundary");
+    if (n == 0) return WL_OK;
+    if (!imgs || !pyramids || !scratch) return fail(WL_EINVAL, "null buffer");
+    if (n > 1 && (img_stride < static_cast<long>(w) * h || pyr_stride < static_cast<long>(w) * h))
+        return fail(WL_EINVAL, "batch stride too small");
+    const size_t q1 = static_cast<size_t>(w / 2) * (h / 2);
+    float* ping[2] = {scratch, scratch + static_cast<size_t>(n) * q1};
+    long offs[32];
+    long off = 0;
+    for (int l = 0; l < levels; ++l) {
+        offs[l] = off;
+        off += 3 * static_cast<long>(w >> (l + 1)) * (h >> (l + 1));
+    }
+    const float* ll = pyramids + off;  // coarsest LL
+    long ll_stride = pyr_stride;
+    for (int l = levels - 1; l >= 0; --l) {
+        const int qw = w >> (l + 1), qh = h >> (l + 1);
+        const long np = static_cast<long>(qw) * qh;
+        const float* hl = pyramids + offs[l];
+        WlLevel L{};
+        L.in[0] = ll;
+        L.in[1] = hl;
+        L.in[2] = hl + np;
+        L.in[3] = hl + 2 * np;
+        L.out[0] = l == 0 ? imgs : ping[(l - 1) & 1];
+        L.qw = qw;
+        L.qh = qh;
+        L.in_pitch = qw;
+        L.out_pitch = 2 * qw;
+        L.wavelet = wavelet;
+        L.scheme = scheme;
+        L.direction = 1;
+        L.prog = prog_index(wavelet, scheme, 1);
+        L.boundary = boundary;
+        L.scaling = undo_scaling != 0;
+        L.nb = n;
+        L.in_bstride[0] = ll_stride;
+        L.in_bstride[1] = L.in_bstride[2] = L.in_bstride[3] = pyr_stride;
+        L.out_bstride[0] = l == 0 ? img_stride : 4 * np;
+        const int st = launch_level_batch(L, static_cast<cudaStream_t>(stream));
+        if (st != WL_OK) return st;
+        ll = L.out[0];
+        ll_stride = L.out_bstride[0];
     }
     return WL_OK;
 }

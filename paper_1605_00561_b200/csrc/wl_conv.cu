@@ -52,6 +52,8 @@ struct ConvArgs {
     float scale;
     int vec4;     // output pitch/pointers allow float4 stores
     int has_map;  // TMA descriptor valid (else every tile takes the LDG path)
+    long in_bstride, out_bstride[4];  // batch: elements between images (blockIdx.z)
+    int ylo, yhi;                  // stored quad rows [ylo, yhi); out[] addresses row ylo
 };
 
 template <class C>
@@ -62,7 +64,9 @@ __global__ void __launch_bounds__(NT) conv_fast_kernel(const __grid_constant__ C
     float* px = reinterpret_cast<float*>(smem_raw);
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw + G::kBytes);
     const int w = 2 * a.qw, h = 2 * a.qh;
-    const int r0 = blockIdx.y * TQY, c0 = blockIdx.x * TQX;
+    const int r0 = a.ylo + blockIdx.y * TQY, c0 = blockIdx.x * TQX;
+    const int b = blockIdx.z;
+    const float* img = a.img + b * a.in_bstride;
     const int py0 = 2 * r0 + C::kRow0, px0 = 2 * c0 - MARGIN;
     const bool interior = a.has_map && py0 >= 0 && px0 >= 0 && py0 + G::kRows <= h &&
                           px0 + SW <= w;
@@ -71,7 +75,7 @@ __global__ void __launch_bounds__(NT) conv_fast_kernel(const __grid_constant__ C
             wlfast::mbar_init(bar, 1);
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
             wlfast::mbar_expect_tx(bar, G::kBytes);
-            wlfast::tma_load_2d(px, &m, bar, px0, py0);
+            wlfast::tma_load_3d(px, &m, bar, px0, py0, b);
         }
         __syncthreads();  // barrier init visible before anyone waits on it
         wlfast::mbar_wait(bar, 0);
@@ -79,7 +83,7 @@ __global__ void __launch_bounds__(NT) conv_fast_kernel(const __grid_constant__ C
         for (int i = threadIdx.x; i < G::kRows * SW; i += NT) {
             const int y = i / SW, x = i - (i / SW) * SW;
             const int ry = resolve(py0 + y, h, a.boundary), rx = resolve(px0 + x, w, a.boundary);
-            px[i] = a.img[(long)ry * a.in_pitch + rx];
+            px[i] = img[(long)ry * a.in_pitch + rx];
         }
         __syncthreads();  // the single data-availability barrier
     }
@@ -87,8 +91,8 @@ __global__ void __launch_bounds__(NT) conv_fast_kernel(const __grid_constant__ C
     constexpr int kBlocksX = TQX / Q;
 #pragma unroll
     for (int k = 0; k < (TQY * kBlocksX) / NT; ++k) {
-        const int b = threadIdx.x + k * NT;
-        const int qr = b / kBlocksX, qb = b - (b / kBlocksX) * kBlocksX;
+        const int blk = threadIdx.x + k * NT;
+        const int qr = blk / kBlocksX, qb = blk - (blk / kBlocksX) * kBlocksX;
         float acc[Q][4];
 #pragma unroll
         for (int q = 0; q < Q; ++q)
@@ -109,7 +113,7 @@ __global__ void __launch_bounds__(NT) conv_fast_kernel(const __grid_constant__ C
             C::template row<Y, Q>(seg, acc);
         });
         const int gy = r0 + qr, gx = c0 + Q * qb;
-        if (gy >= a.qh) continue;
+        if (gy >= a.yhi) continue;
         if (a.scaling) {
 #pragma unroll
             for (int q = 0; q < Q; ++q) {
@@ -117,10 +121,10 @@ __global__ void __launch_bounds__(NT) conv_fast_kernel(const __grid_constant__ C
                 acc[q][3] /= a.scale;
             }
         }
-        const long off = (long)gy * a.out_pitch + gx;
+        const long off = (long)(gy - a.ylo) * a.out_pitch + gx;
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-            float* p = a.out[c] + off;
+            float* p = a.out[c] + b * a.out_bstride[c] + off;
             if (a.vec4 && gx + Q <= a.qw) {
                 *reinterpret_cast<float4*>(p) =
                     make_float4(acc[0][c], acc[1][c], acc[2][c], acc[3][c]);
@@ -149,9 +153,16 @@ cudaError_t launch_conv(const WlLevel& L, cudaStream_t stream) {
     a.scale = P.scale;
     bool v4 = (L.out_pitch % 4) == 0;
     for (int k = 0; k < 4; ++k) v4 = v4 && (reinterpret_cast<uintptr_t>(L.out[k]) % 16) == 0;
+    for (int k = 0; k < 4; ++k) v4 = v4 && ((L.nb > 1 ? L.out_bstride[k] : 0) % 4) == 0;
     a.vec4 = v4;
     CUtensorMap m{};
-    a.has_map = wlfast::make_map(&m, L.in[0], 2 * L.qw, 2 * L.qh, L.in_pitch, SW, G::kRows);
+    const int nb = L.nb > 1 ? L.nb : 1;
+    a.in_bstride = nb > 1 ? L.in_bstride[0] : 0;
+    for (int k = 0; k < 4; ++k) a.out_bstride[k] = nb > 1 ? L.out_bstride[k] : 0;
+    a.ylo = L.yhi > 0 ? L.ylo : 0;
+    a.yhi = L.yhi > 0 ? L.yhi : L.qh;
+    a.has_map = wlfast::make_map(&m, L.in[0], 2 * L.qw, 2 * L.qh, L.in_pitch, nb, a.in_bstride,
+                                 SW, G::kRows);
     const size_t smem = G::kBytes + 16;
     static bool attr[64] = {};
     int dev = 0;
@@ -161,7 +172,7 @@ cudaError_t launch_conv(const WlLevel& L, cudaStream_t stream) {
                              (int)smem);
         attr[dev & 63] = true;
     }
-    const dim3 grid((L.qw + TQX - 1) / TQX, (L.qh + TQY - 1) / TQY);
+    const dim3 grid((L.qw + TQX - 1) / TQX, (a.yhi - a.ylo + TQY - 1) / TQY, nb);
     conv_fast_kernel<C><<<grid, NT, smem, stream>>>(m, a);
     wl_count_launch();
     return cudaGetLastError();

@@ -20,16 +20,21 @@ EncodeTiledFn encode_fn() {
     return fn;
 }
 
-bool make_map(CUtensorMap* m, const float* base, int w, int h, long pitch, int box_w,
-              int box_h) {
+bool make_map(CUtensorMap* m, const float* base, int w, int h, long pitch, int nb, long bstride,
+              int box_w, int box_h) {
     EncodeTiledFn enc = encode_fn();
     if (!enc) return false;
-    if ((reinterpret_cast<uintptr_t>(base) & 15) || ((pitch * 4) & 15)) return false;
-    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(w), static_cast<cuuint64_t>(h)};
-    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(pitch) * 4};
-    const cuuint32_t box[2] = {static_cast<cuuint32_t>(box_w), static_cast<cuuint32_t>(box_h)};
-    const cuuint32_t es[2] = {1, 1};
-    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides,
+    if (nb < 1) nb = 1;
+    if (nb == 1) bstride = pitch * static_cast<long>(h);  // any valid stride
+    if ((reinterpret_cast<uintptr_t>(base) & 15) || ((pitch * 4) & 15) || ((bstride * 4) & 15))
+        return false;
+    const cuuint64_t dims[3] = {static_cast<cuuint64_t>(w), static_cast<cuuint64_t>(h),
+                                static_cast<cuuint64_t>(nb)};
+    const cuuint64_t strides[2] = {static_cast<cuuint64_t>(pitch) * 4,
+                                   static_cast<cuuint64_t>(bstride) * 4};
+    const cuuint32_t box[3] = {static_cast<cuuint32_t>(box_w), static_cast<cuuint32_t>(box_h), 1};
+    const cuuint32_t es[3] = {1, 1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides,
                box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
@@ -76,6 +81,9 @@ bool wl_fast_supported(const WlLevel& L) {
         if ((L.in_pitch % 4) != 0 || !aligned(L.out[0], 16) || (L.out_pitch % 4) != 0)
             return false;
     }
+    if (L.nb > 1)
+        for (int k = 0; k < 4; ++k)
+            if ((L.in_bstride[k] % 4) != 0 || (L.out_bstride[k] % 4) != 0) return false;
     int R, NW;
     geometry(L, &R, &NW);
     const int H = wl_host_program(L.prog).halo;
@@ -101,11 +109,23 @@ cudaError_t wl_launch_fast(const WlLevel& L, cudaStream_t stream) {
     // to the interpreter, which mirrors every out-of-image read per step.
     const int Y0 = plan.args.Y0, X0 = plan.args.X0;
     const int Y1 = Y0 + plan.tiles_y * plan.args.TH, X1 = X0 + plan.args.tiles_x * plan.args.TW;
+    if (L.yhi > 0) return cudaErrorNotSupported;  // windows are periodic-only
     WlRects fr{};
     fr.n = 4;
     fr.y0[0] = 0;  fr.x0[0] = 0;  fr.ny[0] = Y0;          fr.nx[0] = L.qw;       // top
     fr.y0[1] = Y1; fr.x0[1] = 0;  fr.ny[1] = L.qh - Y1;   fr.nx[1] = L.qw;       // bottom
     fr.y0[2] = Y0; fr.x0[2] = 0;  fr.ny[2] = Y1 - Y0;     fr.nx[2] = X0;         // left
     fr.y0[3] = Y0; fr.x0[3] = X1; fr.ny[3] = Y1 - Y0;     fr.nx[3] = L.qw - X1;  // right
-    return wl_launch_interp_rects(L, fr, stream);
+    const int nb = L.nb > 1 ? L.nb : 1;
+    for (int b = 0; b < nb; ++b) {  // the frame of every image of a batch
+        WlLevel Li = L;
+        Li.nb = 1;
+        for (int k = 0; k < 4; ++k) {
+            if (Li.in[k]) Li.in[k] += b * L.in_bstride[k];
+            if (Li.out[k]) Li.out[k] += b * L.out_bstride[k];
+        }
+        e = wl_launch_interp_rects(Li, fr, stream);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
 }

@@ -91,6 +91,15 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
         "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
         : "memory");
 }
+// 3-D box (x, y, image of a batch).
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int x, int y, int z) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+        : "memory");
+}
 // Producer-side wait: the TMA warp is normally far ahead of the compute
 // warps, so poll with exponential back-off instead of a tight spin that
 // steals issue slots from the compute warps sharing its scheduler.
@@ -122,13 +131,16 @@ struct FastArgs {
     float* out[4];       // fwd: LL, HL, LH, HH planes; inv: out[0] = image
     long out_pitch;      // elements
     int qw, qh;          // component-grid size
-    int tiles_x, ntiles;
-    int t0;              // index of the first tile row/column (-1 when covering borders)
+    int tiles_x, ntiles; // ntiles = images x tiles per image
+    int ntiles_img;      // tiles per image
+    int tx0, ty0;        // index of the first tile column / row (-1 when covering borders)
     int X0, Y0;          // first output cell of tile (0, 0)
     int TW, TH;          // output tile size in cells
     int wrap;            // periodic plan covering the whole image (border tiles wrap)
     int scaling;
     float scale;
+    long in_bstride[4], out_bstride[4];  // per plane: elements between images of a batch
+    int ylo, yhi;        // stored cell rows [ylo, yhi); out[] addresses row ylo
 };
 
 template <int R, int NW>
@@ -208,20 +220,21 @@ __global__ void __launch_bounds__((NW + 1) * 32, 2)
             for (int i = 0, t = blockIdx.x; t < a.ntiles; t += gridDim.x, ++i) {
                 const int s = i & 1;
                 if (i >= 2) mbar_wait_backoff(&empty[s], ((i >> 1) - 1) & 1);
-                const int tyi = t / a.tiles_x;
-                const int ty = tyi + a.t0, tx = t - tyi * a.tiles_x + a.t0;
+                const int b = t / a.ntiles_img, tt = t - b * a.ntiles_img;
+                const int tyi = tt / a.tiles_x;
+                const int ty = tyi + a.ty0, tx = tt - tyi * a.tiles_x + a.tx0;
                 const int cx = a.X0 + tx * a.TW - H;      // first compute cell column
                 const int cy = a.Y0 + ty * a.TH - H - 1;  // ghost row above the region
                 float* dst = stage + s * G::kStageFloats;
                 mbar_expect_tx(&full[s], G::kStageBytes);
                 if (DIR == 0) {
-                    tma_load_2d(dst, &m0, &full[s], 2 * cx, 2 * cy);
+                    tma_load_3d(dst, &m0, &full[s], 2 * cx, 2 * cy, b);
                 } else {
                     constexpr int plane = TWC * G::kRows;
-                    tma_load_2d(dst, &m0, &full[s], cx, cy);
-                    tma_load_2d(dst + plane, &m1, &full[s], cx, cy);
-                    tma_load_2d(dst + 2 * plane, &m2, &full[s], cx, cy);
-                    tma_load_2d(dst + 3 * plane, &m3, &full[s], cx, cy);
+                    tma_load_3d(dst, &m0, &full[s], cx, cy, b);
+                    tma_load_3d(dst + plane, &m1, &full[s], cx, cy, b);
+                    tma_load_3d(dst + 2 * plane, &m2, &full[s], cx, cy, b);
+                    tma_load_3d(dst + 3 * plane, &m3, &full[s], cx, cy, b);
                 }
             }
         }
@@ -236,8 +249,9 @@ __global__ void __launch_bounds__((NW + 1) * 32, 2)
 
     for (int i = 0, t = blockIdx.x; t < a.ntiles; t += gridDim.x, ++i) {
         const int s = i & 1;
-        const int tyi = t / a.tiles_x;
-        const int ty = tyi + a.t0, tx = t - tyi * a.tiles_x + a.t0;
+        const int b = t / a.ntiles_img, tt = t - b * a.ntiles_img;
+        const int tyi = tt / a.tiles_x;
+        const int ty = tyi + a.ty0, tx = tt - tyi * a.tiles_x + a.tx0;
         const int cx = a.X0 + tx * a.TW - H;      // first compute cell column
         const int cy = a.Y0 + ty * a.TH - H - 1;  // ghost row above the region
         // Periodic border tile (only when the plan covers the whole image):
@@ -260,14 +274,16 @@ __global__ void __launch_bounds__((NW + 1) * 32, 2)
                     int rx = (cx + CPT * lane + j) % a.qw;
                     rx += rx < 0 ? a.qw : 0;
                     if (DIR == 0) {
-                        const float* p = a.in[0] + (long)(2 * ry) * a.in_pitch + 2 * rx;
+                        const float* p =
+                            a.in[0] + b * a.in_bstride[0] + (long)(2 * ry) * a.in_pitch + 2 * rx;
                         dst[j][0] = p[0];
                         dst[j][1] = p[1];
                         dst[j][2] = p[a.in_pitch];
                         dst[j][3] = p[a.in_pitch + 1];
                     } else {
 #pragma unroll
-                        for (int c = 0; c < 4; ++c) dst[j][c] = a.in[c][(long)ry * a.in_pitch + rx];
+                        for (int c = 0; c < 4; ++c)
+                            dst[j][c] = a.in[c][b * a.in_bstride[c] + (long)ry * a.in_pitch + rx];
                     }
                 }
             } else if (DIR == 0) {
@@ -433,16 +449,16 @@ __global__ void __launch_bounds__((NW + 1) * 32, 2)
         }
         // 64-bit row pointers of the lane's first cell, advanced per row
         float* pk[4];
-        const long off0 = DIR == 0 ? (long)gy0 * a.out_pitch + gx
-                                   : (long)(2 * gy0) * a.out_pitch + 2 * gx;
+        const long off0 = DIR == 0 ? (long)(gy0 - a.ylo) * a.out_pitch + gx
+                                   : (long)(2 * (gy0 - a.ylo)) * a.out_pitch + 2 * gx;
 #pragma unroll
-        for (int k = 0; k < (DIR == 0 ? 4 : 1); ++k) pk[k] = a.out[k] + off0;
+        for (int k = 0; k < (DIR == 0 ? 4 : 1); ++k) pk[k] = a.out[k] + b * a.out_bstride[k] + off0;
         const long step = DIR == 0 ? a.out_pitch : 2 * a.out_pitch;
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             const int qr = warp * R + r;
             const int gy = gy0 + r;
-            const bool row_ok = qr >= H && qr < H + a.TH && gy >= 0 && gy < a.qh;
+            const bool row_ok = qr >= H && qr < H + a.TH && gy >= a.ylo && gy < a.yhi;
             if (DIR == 0) {
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
@@ -481,7 +497,10 @@ using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t
                                    CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 EncodeTiledFn encode_fn();
 
-bool make_map(CUtensorMap* m, const float* base, int w, int h, long pitch, int box_w, int box_h);
+// 3-D map (w, h, nb images at `bstride` elements apart) of a float32 buffer;
+// box = box_w x box_h x 1.
+bool make_map(CUtensorMap* m, const float* base, int w, int h, long pitch, int nb, long bstride,
+              int box_w, int box_h);
 
 // Launch configuration per wavelet: (R, NW).
 template <int WAVELET>
@@ -521,8 +540,15 @@ struct Plan {
 //    the top/left, t0 = -1); border tiles load wrapped cells (exact).
 //  * symmetric: only tiles whose compute region lies inside the image; the
 //    frame around them is the interpreter's (per-step mirroring).
+//  * strip window (L.yhi > 0, periodic only): tile rows cover the stored rows
+//    [ylo, yhi) only; the rows around them are halo rows physically present
+//    in the buffer (ylo >= H + 1 and yhi <= qh - H - 1 keep every stored
+//    cell's dependency cone and the tiles' ghost rows inside the buffer).
 inline Plan plan_tiles(const WlLevel& L, int H, int R, int NW) {
     Plan p{};
+    const int nb = L.nb > 1 ? L.nb : 1;
+    p.args.ylo = 0;
+    p.args.yhi = L.qh;
     // TMA requires the innermost box start to be 16-byte aligned: the inverse
     // boxes start at cell column X0 - H + tx*TW of a float32 plane, so TW is
     // rounded down to a multiple of 4 there (the forward starts at pixel
@@ -531,28 +557,41 @@ inline Plan plan_tiles(const WlLevel& L, int H, int R, int NW) {
     const int TH = NW * R - 2 * H;
     const int X0 = H, Y0 = H + 1;
     int tx, ty;
-    if (L.boundary == 0) {
+    int y0 = Y0;
+    if (L.yhi > 0) {
+        if (L.boundary != 0 || L.ylo < H + 1 || L.yhi > L.qh - H - 1 || L.yhi <= L.ylo)
+            return p;  // ok = false
+        tx = (L.qw - X0 > 0 ? (L.qw - X0 + TW - 1) / TW : 0) + 1;
+        ty = (L.yhi - L.ylo + TH - 1) / TH;
+        y0 = L.ylo;
+        p.args.tx0 = -1;
+        p.args.ty0 = 0;
+        p.args.wrap = 1;
+        p.args.ylo = L.ylo;
+        p.args.yhi = L.yhi;
+    } else if (L.boundary == 0) {
         tx = (L.qw - X0 > 0 ? (L.qw - X0 + TW - 1) / TW : 0) + 1;
         ty = (L.qh - Y0 > 0 ? (L.qh - Y0 + TH - 1) / TH : 0) + 1;
-        p.args.t0 = -1;
+        p.args.tx0 = p.args.ty0 = -1;
         p.args.wrap = 1;
     } else {
         tx = L.qw >= TWC ? (L.qw - TWC) / TW + 1 : 0;
         const int span = L.qh - (Y0 - H - 1);  // rows available from the first ghost row
         ty = span >= NW * R + 2 ? (span - (NW * R + 2)) / TH + 1 : 0;
-        p.args.t0 = 0;
+        p.args.tx0 = p.args.ty0 = 0;
         p.args.wrap = 0;
     }
     p.args.tiles_x = tx;
     p.tiles_y = ty;
-    p.args.ntiles = tx * ty;
+    p.args.ntiles_img = tx * ty;
+    p.args.ntiles = nb * tx * ty;
     p.args.X0 = X0;
-    p.args.Y0 = Y0;
+    p.args.Y0 = y0;
     p.args.TW = TW;
     p.args.TH = TH;
     p.args.qw = L.qw;
     p.args.qh = L.qh;
-    p.ok = tx > 0 && ty > 0;
+    p.ok = tx > 0 && ty > 0 && (long)nb * tx * ty < (1l << 31);
     return p;
 }
 
@@ -561,14 +600,21 @@ cudaError_t launch(const WlLevel& L, const Plan& plan, cudaStream_t stream) {
     using G = Geometry<R, NW>;
     CUtensorMap maps[4];
     FastArgs a = plan.args;
+    const int nb = L.nb > 1 ? L.nb : 1;
+    for (int k = 0; k < 4; ++k) {
+        a.in_bstride[k] = nb > 1 ? L.in_bstride[k] : 0;
+        a.out_bstride[k] = nb > 1 ? L.out_bstride[k] : 0;
+    }
     if (DIR == 0) {
-        if (!make_map(&maps[0], L.in[0], 2 * L.qw, 2 * L.qh, L.in_pitch, 2 * TWC, 2 * G::kRows))
+        if (!make_map(&maps[0], L.in[0], 2 * L.qw, 2 * L.qh, L.in_pitch, nb, a.in_bstride[0],
+                      2 * TWC, 2 * G::kRows))
             return cudaErrorInvalidValue;
         maps[1] = maps[2] = maps[3] = maps[0];
         for (int k = 0; k < 4; ++k) a.out[k] = L.out[k];
     } else {
         for (int k = 0; k < 4; ++k)
-            if (!make_map(&maps[k], L.in[k], L.qw, L.qh, L.in_pitch, TWC, G::kRows))
+            if (!make_map(&maps[k], L.in[k], L.qw, L.qh, L.in_pitch, nb, a.in_bstride[k], TWC,
+                          G::kRows))
                 return cudaErrorInvalidValue;
         a.out[0] = L.out[0];
         a.out[1] = a.out[2] = a.out[3] = nullptr;

@@ -16,6 +16,15 @@ struct WlLevel {
     int wavelet, scheme, direction;
     int boundary;        // 0 periodic, 1 symmetric
     int scaling;         // apply (fwd) / undo (inv) the zeta^2 scaling step
+    // Batch: nb images (0/1 = one), element strides between consecutive
+    // images of the input / output buffers (every plane of an image shares
+    // its image's offset).
+    int nb;
+    long in_bstride[4], out_bstride[4];
+    // Row window ("strip" mode, fast engine only): only component rows
+    // [ylo, yhi) of the qh-row buffer are produced; out[] points at row ylo.
+    // yhi == 0: the whole plane (out[] at row 0).
+    int ylo, yhi;
 };
 
 const WlProgram& wl_host_program(int prog);
