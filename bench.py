@@ -115,13 +115,20 @@ def dist_init():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # WL_BENCH_DEVICE / WL_BENCH_BACKEND: test hooks to run N ranks on one
+    # GPU (gloo for the timing barrier; NCCL refuses duplicate devices).
+    dev = int(os.environ.get("WL_BENCH_DEVICE", local))
+    backend = os.environ.get("WL_BENCH_BACKEND", "nccl")
     if ws > 1:
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        torch.cuda.set_device(dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(backend)
     else:
-        torch.cuda.set_device(0)
-    return ws, rank, local
+        torch.cuda.set_device(dev)
+    return ws, rank, dev
 
 
 def barrier_max(x, ws):
@@ -130,7 +137,8 @@ def barrier_max(x, ws):
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], device="cuda", dtype=torch.float64)
+    on_gpu = dist.get_backend() == "nccl"
+    t = torch.tensor([x], device="cuda" if on_gpu else "cpu", dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -329,36 +337,37 @@ def run_gpu(args):
     # ---- e2e through the public API with pinned host buffers
     e2e = None
     if args.e2e_steps > 0:
+        # The reference-facing call shape: forward(const Image&) /
+        # inverse(const QuadGrid&) on HOST buffers (wl_dwt2_forward_host /
+        # wl_dwt2_inverse_host: row-chunk pipeline, H2D/kernels/D2H overlap).
         h_img = torch.empty((n, n), dtype=torch.float32, pin_memory=True)
         h_img.copy_(img.cpu())
         h_q = torch.empty((4, n // 2, n // 2), dtype=torch.float32, pin_memory=True)
         h_rec = torch.empty((n, n), dtype=torch.float32, pin_memory=True)
-        d_img = torch.empty_like(img)
 
         def e2e_step():
             for (w, s) in programs:
-                d_img.copy_(h_img, non_blocking=True)          # H2D image
-                wl.forward(d_img, schemes[(w, s)], out=q)
-                h_q.copy_(q, non_blocking=True)                # D2H planes
-                q.copy_(h_q, non_blocking=True)                # H2D planes
-                wl.inverse(q, w, scheme=s, out=rec)
-                h_rec.copy_(rec, non_blocking=True)            # D2H image
-            torch.cuda.synchronize()
+                wl.forward_host(h_img, schemes[(w, s)], out=h_q)    # host image -> host planes
+                wl.inverse_host(h_q, w, scheme=s, out=h_rec)        # host planes -> host image
 
         e2e_step()
-        barrier(ws)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(args.e2e_steps):
-            e2e_step()
-        e1.record(stream)
         torch.cuda.synchronize()
-        ems = barrier_max(e0.elapsed_time(e1) / args.e2e_steps, ws)
+        barrier(ws)
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            e2e_step()  # synchronous calls: results are in host memory on return
+        ems = barrier_max((time.perf_counter() - t0) * 1e3 / args.e2e_steps, ws)
         bytes_img = 4 * n * n
         e2e = {"value": ws * px_step / (ems * 1e-3) / 1e9, "unit": "GPixel/s",
                "ms_per_step": ems, "h2d_bytes_per_step": 2 * len(programs) * bytes_img,
                "d2h_bytes_per_step": 2 * len(programs) * bytes_img,
-               "steps": args.e2e_steps}
+               "steps": args.e2e_steps,
+               "api": "forward_host / inverse_host (pinned host float32 buffers; wall clock "
+                      "around synchronous calls); byte counts are the image/plane tensors, "
+                      "the strip halo rows add <=1.2% H2D"}
+
+    c4 = run_c4(args, wl, ws, rank, peak) if args.c4 else None
+    c5 = run_c5(args, wl, ws, rank, peak) if args.c5 else None
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
@@ -379,12 +388,103 @@ def run_gpu(args):
                            "parallelism": f"independent images, {ws} rank(s)"},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches, "gpu_launches_per_step": launches / args.steps,
-                "clocks": clk.summary(), "c3": c3, "per_scheme": per}
+                "clocks": clk.summary(), "c3": c3, "c4": c4, "c5": c5, "per_scheme": per}
         print(json.dumps(line), flush=True)
     if ws > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
     return 0
+
+
+def _timed(fn, steps, ws, stream):
+    """device time (ms) per call of fn, max over ranks."""
+    import torch
+    barrier(ws)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        fn()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return barrier_max(e0.elapsed_time(e1) / steps, ws)
+
+
+def run_c4(args, wl, ws, rank, peak):
+    """BASELINE configs[3]: cdf97 5-level pyramid of ONE N x N image split in
+    row strips over the ranks, per-level halo exchange over peer memory
+    (StripPyramid). Strong scaling: the image size is fixed."""
+    import torch
+    n, levels = args.c4_size, 5
+    sch = wl.build_scheme("monolithic_star", "cdf97")
+    if ws > 1:
+        sp = wl.strip_pyramid_distributed(None, n, n, levels, sch)
+    else:
+        sp = wl.StripPyramid(n, n, levels, sch)
+    g = torch.Generator(device="cuda").manual_seed(4000 + rank)
+    sp.input.copy_(torch.rand(sp.input.shape, device="cuda", generator=g))
+    out = torch.empty(sp.slice_elems(), device="cuda")
+    stream = torch.cuda.current_stream()
+    for _ in range(3):
+        sp.forward(out)
+    torch.cuda.synchronize()
+    ms = _timed(lambda: sp.forward(out), max(args.steps, 5), ws, stream)
+    sp.check()
+    algo = 8.0 * n * n * sum(4.0 ** -l for l in range(levels))
+    gbs_per_gpu = algo / ws / (ms * 1e-3) / 1e9
+    sp.close()
+    del out
+    return {"workload": f"configs[3]: cdf97 monolithic_star {levels}-level forward pyramid, "
+                        f"{n}x{n} float32, periodic, {ws} row strip(s) of {n // ws} rows, "
+                        "halo rows pushed per level over peer memory (CUDA IPC)",
+            "value": n * n / (ms * 1e-3) / 1e9, "unit": "GPixel/s (input pixels)",
+            "ms": ms, "ns_per_pixel": ms * 1e6 / (n * n), "scaling": "strong",
+            "algorithmic_bytes": algo, "hbm_gbs_per_gpu": gbs_per_gpu,
+            "frac_per_gpu": gbs_per_gpu / peak}
+
+
+def run_c5(args, wl, ws, rank, peak):
+    """BASELINE configs[4]: 4096 images of 4096^2, cdf53 and cdf97
+    monolithic_star 3-level forward, images sharded over ranks (no
+    communication). A resident pool of distinct images is cycled: each rank's
+    share is processed in batched launches of `chunk` images."""
+    import torch
+    total, n, levels = args.c5_images, 4096, 3
+    mine = total // ws
+    chunk = min(64, mine)
+    pool = max(chunk, min(mine, args.c5_pool) // chunk * chunk)
+    g = torch.Generator(device="cuda").manual_seed(5000 + rank)
+    imgs = torch.rand((pool, n, n), device="cuda", generator=g)
+    pyrs = torch.empty((pool, n * n), device="cuda")
+    scratch = torch.empty(wl.lib().wl_pyramid_batch_scratch_elems(n, n, levels, chunk),
+                          device="cuda")
+    stream = torch.cuda.current_stream()
+    res = {}
+    for w in ("cdf53", "cdf97"):
+        sch = wl.build_scheme("monolithic_star", w)
+
+        def job():
+            for c in range(mine // chunk):
+                i = (c * chunk) % pool
+                wl.multi_level_forward_batch(imgs[i:i + chunk], sch, levels,
+                                             out=pyrs[i:i + chunk], scratch=scratch)
+        job()
+        torch.cuda.synchronize()
+        res[w] = _timed(job, max(1, min(args.steps, 3)), ws, stream)
+    del imgs, pyrs, scratch
+    algo = 8.0 * n * n * sum(4.0 ** -l for l in range(levels)) * total
+    out = {"workload": f"configs[4]: {total} images x {n}^2 float32, monolithic_star "
+                       f"{levels}-level forward, cdf53 and cdf97; {mine} images per rank in "
+                       f"batched launches of {chunk}; resident pool of {pool} distinct images "
+                       "per rank cycled (pool > L2)", "scaling": "strong",
+           "unit": "GPixel/s (input pixels, whole job)"}
+    for w, ms in res.items():
+        gbs = algo / ws / (ms * 1e-3) / 1e9
+        out[w] = {"ms": ms, "value": total * n * n / (ms * 1e-3) / 1e9,
+                  "ns_per_pixel": ms * 1e6 / (total * n * n), "hbm_gbs_per_gpu": gbs,
+                  "frac_per_gpu": gbs / peak}
+    out["value"] = 2 * total * n * n / (sum(res.values()) * 1e-3) / 1e9
+    return out
 
 
 def cpu_baseline(args):
@@ -421,6 +521,11 @@ def main():
     ap.add_argument("--ref-size", type=int, default=512)
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-c3", dest="c3", action="store_false")
+    ap.add_argument("--no-c4", dest="c4", action="store_false")
+    ap.add_argument("--no-c5", dest="c5", action="store_false")
+    ap.add_argument("--c4-size", type=int, default=32768)
+    ap.add_argument("--c5-images", type=int, default=4096)
+    ap.add_argument("--c5-pool", type=int, default=256)
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":

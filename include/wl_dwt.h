@@ -165,6 +165,21 @@ int wl_strips_forward(WlStrips* s, float* slice, void* stream);
 int wl_strips_check(WlStrips* s);
 int wl_strips_destroy(WlStrips* s);
 
+/* ------------------------------------------------------------ host buffers
+ * The reference's own call shape: `forward(const Image&)` / `inverse(const
+ * QuadGrid&)` take and return HOST memory (transform.hpp:65-72). These take
+ * float32 host buffers (pitches in elements), run on the current device and
+ * return when the result is in host memory. Periodic cdf53/cdf97 transforms
+ * are pipelined in row chunks (strip transforms on 3 streams: H2D, kernels
+ * and D2H overlap); everything else runs whole-image. Pin the host buffers
+ * (cudaHostAlloc / cudaHostRegister) for asynchronous copies. */
+int wl_dwt2_forward_host(const float* img, int w, int h, long img_pitch, int wavelet, int scheme,
+                         int boundary, int scaling, float* ll, float* hl, float* lh, float* hh,
+                         long plane_pitch);
+int wl_dwt2_inverse_host(const float* ll, const float* hl, const float* lh, const float* hh,
+                         int qw, int qh, long plane_pitch, int wavelet, int scheme, int boundary,
+                         int undo_scaling, float* img, long img_pitch);
+
 /* Engine selection for tests/benchmarks: 0 = auto (fast register-tile engine
  * where available, generic tile interpreter otherwise), 1 = force the generic
  * interpreter, 2 = force the fast engine (WL_EINVAL where unsupported).

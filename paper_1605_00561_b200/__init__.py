@@ -77,6 +77,8 @@ def lib() -> ctypes.CDLL:
         l.wl_strips_forward.argtypes = [vp, fp, vp]
         l.wl_strips_check.argtypes = [vp]
         l.wl_strips_destroy.argtypes = [vp]
+        l.wl_dwt2_forward_host.argtypes = [fp, i, i, lg, i, i, i, i, fp, fp, fp, fp, lg]
+        l.wl_dwt2_inverse_host.argtypes = [fp, fp, fp, fp, i, i, lg, i, i, i, i, fp, lg]
         l.wl_set_engine.argtypes = [i]
         l.wl_launch_count.restype = lg
         _lib = l
@@ -567,3 +569,48 @@ def strip_pyramid_distributed(img_rows, w, h, levels, scheme: Scheme, group=None
     if img_rows is not None:
         sp.input.copy_(img_rows)
     return sp
+
+
+# ------------------------------------------------------------ host buffers
+def _host_f32(t, what):
+    import torch
+    if not isinstance(t, torch.Tensor) or t.is_cuda or t.dtype != torch.float32:
+        raise ValueError(f"{what} must be a float32 CPU tensor")
+    return t.contiguous()
+
+
+def forward_host(img, scheme: Scheme, boundary="periodic", apply_scaling=False, out=None):
+    """`forward` with HOST buffers (the reference's own call shape,
+    transform.hpp:65-66): (h, w) float32 CPU tensor -> (4, h/2, w/2) CPU
+    planes. Copies and kernels are pipelined in row chunks on the current
+    device; pass pinned tensors (`pin_memory()`) for full PCIe overlap."""
+    import torch
+    img = _host_f32(img, "img")
+    if img.dim() != 2:
+        raise ValueError("img must be 2-D (height, width)")
+    h, w = img.shape
+    if out is None:
+        out = torch.empty((4, max(h // 2, 0), max(w // 2, 0)), dtype=torch.float32)
+    _check(lib().wl_dwt2_forward_host(
+        img.data_ptr(), w, h, w, scheme.wavelet.index, scheme.kind,
+        _index(BOUNDARIES, boundary, "boundary"), int(bool(apply_scaling)),
+        out[0].data_ptr(), out[1].data_ptr(), out[2].data_ptr(), out[3].data_ptr(),
+        out.stride(1)))
+    return out
+
+
+def inverse_host(q, wavelet, boundary="periodic", undo_scaling=False, scheme=None, out=None):
+    """`inverse` with HOST buffers: (4, qh, qw) CPU planes -> (2qh, 2qw)."""
+    import torch
+    q = _host_f32(q, "q")
+    if q.dim() != 3 or q.shape[0] != 4:
+        raise ValueError("q must be (4, qh, qw)")
+    w = wavelet if isinstance(wavelet, WaveletSpec) else get_wavelet(wavelet)
+    _, qh, qw = q.shape
+    if out is None:
+        out = torch.empty((2 * qh, 2 * qw), dtype=torch.float32)
+    _check(lib().wl_dwt2_inverse_host(
+        q[0].data_ptr(), q[1].data_ptr(), q[2].data_ptr(), q[3].data_ptr(), qw, qh, qw, w.index,
+        _kind(scheme), _index(BOUNDARIES, boundary, "boundary"), int(bool(undo_scaling)),
+        out.data_ptr(), out.stride(0)))
+    return out

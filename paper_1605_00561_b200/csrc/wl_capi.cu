@@ -98,6 +98,8 @@ int strip_halo(int wavelet, int direction) {
 
 void wl_count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
+int wl_fail(int code, const char* msg) { return fail(code, msg); }
+
 extern "C" {
 
 const char* wl_last_error(void) { return g_err.c_str(); }

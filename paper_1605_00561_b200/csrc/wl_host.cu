@@ -1,0 +1,248 @@
+// Host-buffer entry points: the reference's own call shape (transform.hpp:
+// 65-72: `forward(const Image&)` / `inverse(const QuadGrid&)` take and return
+// host memory), float32 here.
+//
+// Large periodic cdf53/cdf97 transforms are pipelined in row chunks: chunk k
+// is copied host->device (with the halo rows the strip transform needs,
+// wrapped at the image border), transformed by the strip kernels
+// (bit-identical rows of the whole-image transform) and copied back, on one
+// of three streams, so PCIe in both directions and the kernels overlap. Every
+// other case (symmetric boundary, dd137, small or unaligned images) runs
+// whole-image: copy in, transform, copy out. The call returns when the
+// result is in host memory. Host buffers should be pinned
+// (cudaHostRegister / cudaHostAlloc) for the copies to run asynchronously.
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <string>
+
+#include "../../include/wl_dwt.h"
+#include "wl_internal.h"
+
+namespace {
+
+constexpr int kSlots = 3;
+constexpr size_t kChunkBytes = 32u << 20;  // target input bytes per chunk
+
+struct Workspace {
+    int device = -1;
+    cudaStream_t streams[kSlots] = {};
+    cudaEvent_t done[kSlots] = {};
+    float* in[kSlots] = {};
+    float* out[kSlots] = {};
+    size_t in_cap = 0, out_cap = 0;  // floats per slot
+
+    bool ensure(size_t in_floats, size_t out_floats) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (device != dev) {
+            release();
+            device = dev;
+            for (int s = 0; s < kSlots; ++s) {
+                if (cudaStreamCreateWithFlags(&streams[s], cudaStreamNonBlocking) != cudaSuccess)
+                    return false;
+                if (cudaEventCreateWithFlags(&done[s], cudaEventDisableTiming) != cudaSuccess)
+                    return false;
+            }
+        }
+        if (in_floats > in_cap || out_floats > out_cap) {
+            for (int s = 0; s < kSlots; ++s) {
+                cudaFree(in[s]);
+                cudaFree(out[s]);
+                in[s] = out[s] = nullptr;
+            }
+            in_cap = in_floats > in_cap ? in_floats : in_cap;
+            out_cap = out_floats > out_cap ? out_floats : out_cap;
+            for (int s = 0; s < kSlots; ++s) {
+                if (cudaMalloc(&in[s], in_cap * sizeof(float)) != cudaSuccess) return false;
+                if (cudaMalloc(&out[s], out_cap * sizeof(float)) != cudaSuccess) return false;
+            }
+        }
+        return true;
+    }
+    void release() {
+        if (device < 0) return;
+        for (int s = 0; s < kSlots; ++s) {
+            cudaFree(in[s]);
+            cudaFree(out[s]);
+            if (streams[s]) cudaStreamDestroy(streams[s]);
+            if (done[s]) cudaEventDestroy(done[s]);
+            in[s] = out[s] = nullptr;
+            streams[s] = nullptr;
+            done[s] = nullptr;
+        }
+        in_cap = out_cap = 0;
+        device = -1;
+    }
+};
+
+thread_local Workspace g_ws;
+
+int herr(int code, const std::string& m) { return wl_fail(code, m.c_str()); }
+
+int cuda_err(cudaError_t e, const char* where) {
+    return herr(WL_ERUNTIME, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+// Copy host rows [r0, r1) of a periodic image (rows wrap mod h) into
+// consecutive device rows.
+cudaError_t rows_h2d(float* dst, long dpitch, const float* src, long spitch, int w, int h, int r0,
+                     int r1, cudaStream_t s) {
+    int r = r0;
+    while (r < r1) {
+        int rr = r % h;
+        rr += rr < 0 ? h : 0;
+        const int n = (r1 - r) < (h - rr) ? (r1 - r) : (h - rr);
+        cudaError_t e = cudaMemcpy2DAsync(dst + static_cast<long>(r - r0) * dpitch, dpitch * 4,
+                                          src + static_cast<long>(rr) * spitch, spitch * 4, w * 4,
+                                          n, cudaMemcpyHostToDevice, s);
+        if (e != cudaSuccess) return e;
+        r += n;
+    }
+    return cudaSuccess;
+}
+
+int chunk_rows(long row_bytes, int total, int align) {
+    long r = static_cast<long>(kChunkBytes) / (row_bytes > 0 ? row_bytes : 1);
+    r = r < 64 ? 64 : r;
+    r -= r % align;
+    return r >= total ? total : static_cast<int>(r);
+}
+
+}  // namespace
+
+extern "C" {
+
+int wl_dwt2_forward_host(const float* img, int w, int h, long img_pitch, int wavelet, int scheme,
+                         int boundary, int scaling, float* ll, float* hl, float* lh, float* hh,
+                         long plane_pitch) {
+    if (w <= 0 || h <= 0 || w % 2 != 0 || h % 2 != 0)
+        return herr(WL_EINVAL, "forward requires even positive dimensions");
+    if (!img || !ll || !hl || !lh || !hh) return herr(WL_EINVAL, "null buffer");
+    if (img_pitch < w || plane_pitch < w / 2) return herr(WL_EINVAL, "pitch too small");
+    const int qw = w / 2;
+    float* hp[4] = {ll, hl, lh, hh};
+    const int halo = (wavelet == WL_CDF53 || wavelet == WL_CDF97)
+                         ? wl_strip_halo_rows(wavelet, scheme, 0) : -1;
+    const bool chunked = boundary == WL_PERIODIC && halo > 0 && (w % 4) == 0 && h >= 2 * halo &&
+                         scheme >= 0 && scheme <= 9;
+    const int R = chunked ? chunk_rows(4L * w, h, 2) : h;
+    if (!chunked || R >= h) {
+        // whole image: one slot, copy in / transform / copy out
+        const size_t nin = static_cast<size_t>(w) * h, nout = 4 * static_cast<size_t>(qw) * (h / 2);
+        if (!g_ws.ensure(nin, nout)) return herr(WL_ERUNTIME, "device workspace allocation failed");
+        cudaStream_t s = g_ws.streams[0];
+        float* d = g_ws.in[0];
+        cudaError_t e = cudaMemcpy2DAsync(d, w * 4, img, img_pitch * 4, w * 4, h,
+                                          cudaMemcpyHostToDevice, s);
+        if (e != cudaSuccess) return cuda_err(e, "H2D");
+        const size_t np = static_cast<size_t>(qw) * (h / 2);
+        float* o = g_ws.out[0];
+        int st = wl_dwt2_forward(d, w, h, w, wavelet, scheme, boundary, scaling, o, o + np,
+                                 o + 2 * np, o + 3 * np, qw, s);
+        if (st != WL_OK) return st;
+        for (int c = 0; c < 4; ++c) {
+            e = cudaMemcpy2DAsync(hp[c], plane_pitch * 4, o + c * np, qw * 4, qw * 4, h / 2,
+                                  cudaMemcpyDeviceToHost, s);
+            if (e != cudaSuccess) return cuda_err(e, "D2H");
+        }
+        e = cudaStreamSynchronize(s);
+        return e == cudaSuccess ? WL_OK : cuda_err(e, "forward_host");
+    }
+    const size_t nin = static_cast<size_t>(w) * (R + 2 * halo);
+    const size_t np = static_cast<size_t>(qw) * (R / 2);
+    if (!g_ws.ensure(nin, 4 * np)) return herr(WL_ERUNTIME, "device workspace allocation failed");
+    int k = 0;
+    for (int r0 = 0; r0 < h; r0 += R, ++k) {
+        const int s = k % kSlots;
+        cudaStream_t st = g_ws.streams[s];
+        const int r1 = r0 + R < h ? r0 + R : h;
+        const int rows = r1 - r0;
+        cudaError_t e = rows_h2d(g_ws.in[s], w, img, img_pitch, w, h, r0 - halo, r1 + halo, st);
+        if (e != cudaSuccess) return cuda_err(e, "H2D");
+        float* o = g_ws.out[s];
+        const size_t npc = static_cast<size_t>(qw) * (rows / 2);
+        const int r = wl_dwt2_forward_strip(g_ws.in[s] + static_cast<size_t>(halo) * w, w, rows,
+                                            halo, w, wavelet, scheme, scaling, o, o + npc,
+                                            o + 2 * npc, o + 3 * npc, qw, st);
+        if (r != WL_OK) return r;
+        for (int c = 0; c < 4; ++c) {
+            e = cudaMemcpy2DAsync(hp[c] + static_cast<long>(r0 / 2) * plane_pitch,
+                                  plane_pitch * 4, o + c * npc, qw * 4, qw * 4, rows / 2,
+                                  cudaMemcpyDeviceToHost, st);
+            if (e != cudaSuccess) return cuda_err(e, "D2H");
+        }
+    }
+    for (int s = 0; s < kSlots; ++s) {
+        cudaError_t e = cudaStreamSynchronize(g_ws.streams[s]);
+        if (e != cudaSuccess) return cuda_err(e, "forward_host");
+    }
+    return WL_OK;
+}
+
+int wl_dwt2_inverse_host(const float* ll, const float* hl, const float* lh, const float* hh,
+                         int qw, int qh, long plane_pitch, int wavelet, int scheme, int boundary,
+                         int undo_scaling, float* img, long img_pitch) {
+    if (qw <= 0 || qh <= 0) return herr(WL_EINVAL, "inverse requires positive plane dimensions");
+    if (!img || !ll || !hl || !lh || !hh) return herr(WL_EINVAL, "null buffer");
+    if (img_pitch < 2 * qw || plane_pitch < qw) return herr(WL_EINVAL, "pitch too small");
+    const float* hp[4] = {ll, hl, lh, hh};
+    const int halo = (wavelet == WL_CDF53 || wavelet == WL_CDF97)
+                         ? wl_strip_halo_rows(wavelet, scheme, 1) : -1;
+    const bool chunked = boundary == WL_PERIODIC && halo > 0 && (qw % 4) == 0 &&
+                         qh >= 2 * halo && scheme >= 0 && scheme <= 9;
+    const int R = chunked ? chunk_rows(16L * qw, qh, 1) : qh;
+    if (!chunked || R >= qh) {
+        const size_t np = static_cast<size_t>(qw) * qh;
+        if (!g_ws.ensure(4 * np, 4 * np))
+            return herr(WL_ERUNTIME, "device workspace allocation failed");
+        cudaStream_t s = g_ws.streams[0];
+        float* d = g_ws.in[0];
+        for (int c = 0; c < 4; ++c) {
+            cudaError_t e = cudaMemcpy2DAsync(d + c * np, qw * 4, hp[c], plane_pitch * 4, qw * 4,
+                                              qh, cudaMemcpyHostToDevice, s);
+            if (e != cudaSuccess) return cuda_err(e, "H2D");
+        }
+        float* o = g_ws.out[0];
+        int st = wl_dwt2_inverse(d, d + np, d + 2 * np, d + 3 * np, qw, qh, qw, wavelet, scheme,
+                                 boundary, undo_scaling, o, 2 * qw, s);
+        if (st != WL_OK) return st;
+        cudaError_t e = cudaMemcpy2DAsync(img, img_pitch * 4, o, 2 * qw * 4, 2 * qw * 4, 2 * qh,
+                                          cudaMemcpyDeviceToHost, s);
+        if (e != cudaSuccess) return cuda_err(e, "D2H");
+        e = cudaStreamSynchronize(s);
+        return e == cudaSuccess ? WL_OK : cuda_err(e, "inverse_host");
+    }
+    const size_t npb = static_cast<size_t>(qw) * (R + 2 * halo);  // one plane buffer
+    if (!g_ws.ensure(4 * npb, static_cast<size_t>(4) * qw * R))
+        return herr(WL_ERUNTIME, "device workspace allocation failed");
+    int k = 0;
+    for (int q0 = 0; q0 < qh; q0 += R, ++k) {
+        const int s = k % kSlots;
+        cudaStream_t st = g_ws.streams[s];
+        const int q1 = q0 + R < qh ? q0 + R : qh;
+        const int rows = q1 - q0;
+        const size_t pb = static_cast<size_t>(qw) * (rows + 2 * halo);
+        for (int c = 0; c < 4; ++c) {
+            cudaError_t e = rows_h2d(g_ws.in[s] + c * pb, qw, hp[c], plane_pitch, qw, qh,
+                                     q0 - halo, q1 + halo, st);
+            if (e != cudaSuccess) return cuda_err(e, "H2D");
+        }
+        float* d = g_ws.in[s] + static_cast<size_t>(halo) * qw;
+        const int r = wl_dwt2_inverse_strip(d, d + pb, d + 2 * pb, d + 3 * pb, qw, rows, halo, qw,
+                                            wavelet, scheme, undo_scaling, g_ws.out[s], 2 * qw,
+                                            st);
+        if (r != WL_OK) return r;
+        cudaError_t e = cudaMemcpy2DAsync(img + static_cast<long>(2 * q0) * img_pitch,
+                                          img_pitch * 4, g_ws.out[s], 2 * qw * 4, 2 * qw * 4,
+                                          2 * rows, cudaMemcpyDeviceToHost, st);
+        if (e != cudaSuccess) return cuda_err(e, "D2H");
+    }
+    for (int s = 0; s < kSlots; ++s) {
+        cudaError_t e = cudaStreamSynchronize(g_ws.streams[s]);
+        if (e != cudaSuccess) return cuda_err(e, "inverse_host");
+    }
+    return WL_OK;
+}
+
+}  // extern "C"

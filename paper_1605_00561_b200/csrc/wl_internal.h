@@ -51,3 +51,5 @@ cudaError_t wl_launch_fast(const WlLevel& L, cudaStream_t stream);
 bool wl_fast_supported(const WlLevel& L);
 
 void wl_count_launch();
+// Records `msg` as this thread's wl_last_error() and returns `code`.
+int wl_fail(int code, const char* msg);

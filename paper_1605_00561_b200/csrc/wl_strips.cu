@@ -136,12 +136,7 @@ __global__ void wait_kernel(const unsigned* a, const unsigned* b, unsigned epoch
     wait_flags(a, b, epoch, err);
 }
 
-thread_local std::string g_serr;
-
-int sfail(int code, const std::string& m) {
-    g_serr = m;
-    return code;
-}
+int sfail(int code, const std::string& m) { return wl_fail(code, m.c_str()); }
 
 }  // namespace
 
@@ -168,7 +163,7 @@ struct WlStrips {
 
 extern "C" {
 
-const char* wl_strips_last_error(void) { return g_serr.c_str(); }
+const char* wl_strips_last_error(void) { return wl_last_error(); }
 
 size_t wl_strips_blob_bytes(void) { return sizeof(Blob); }
 
@@ -338,7 +333,7 @@ int wl_strips_forward(WlStrips* s, float* slice, void* stream) {
                                  : s->lvl(s->window, l + 1) + static_cast<size_t>(halo) * qw;
         const int r = wl_dwt2_forward_strip(interior, wl_, sl_, halo, wl_, s->wavelet, s->scheme,
                                             s->scaling, ll, hl, hl + np, hl + 2 * np, qw, stream);
-        if (r != WL_OK) return sfail(r, std::string("level transform: ") + wl_last_error());
+        if (r != WL_OK) return r;
     }
     signal_kernel<<<1, 1, 0, st>>>(fu + 2 * L + 1, fd + 2 * L, e);
     wl_count_launch();
