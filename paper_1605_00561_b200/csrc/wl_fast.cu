@@ -53,14 +53,19 @@ cudaError_t wl_fast_cdf97_inv(int scheme, const WlLevel& L, const wlfast::Plan& 
 
 namespace {
 
-void geometry(const WlLevel& L, int* R, int* NW) {
-    if (L.wavelet == 0) {
-        *R = wlfast::Config<0>::R;
-        *NW = wlfast::Config<0>::NW;
-    } else {
-        *R = wlfast::Config<1>::R;
-        *NW = wlfast::Config<1>::NW;
-    }
+template <class C>
+void geo(int* R, int* NW, int* CPT) {
+    *R = C::R;
+    *NW = C::NW;
+    *CPT = C::CPT;
+}
+
+void geometry(const WlLevel& L, int* R, int* NW, int* CPT) {
+    using namespace wlfast;
+    if (L.wavelet == 0)
+        L.direction == 0 ? geo<Config<0, 0>>(R, NW, CPT) : geo<Config<0, 1>>(R, NW, CPT);
+    else
+        L.direction == 0 ? geo<Config<1, 0>>(R, NW, CPT) : geo<Config<1, 1>>(R, NW, CPT);
 }
 
 bool aligned(const void* p, int bytes) { return (reinterpret_cast<uintptr_t>(p) % bytes) == 0; }
@@ -84,18 +89,25 @@ bool wl_fast_supported(const WlLevel& L) {
     if (L.nb > 1)
         for (int k = 0; k < 4; ++k)
             if ((L.in_bstride[k] % 4) != 0 || (L.out_bstride[k] % 4) != 0) return false;
-    int R, NW;
-    geometry(L, &R, &NW);
+    int R, NW, CPT;
+    geometry(L, &R, &NW, &CPT);
+    // CPT = 4 stores aligned float4 groups: plane widths and pitches in
+    // multiples of 4 cells, 16-byte aligned outputs
+    if (CPT == 4) {
+        if (L.qw % 4 != 0 || L.out_pitch % 4 != 0) return false;
+        for (int k = 0; k < (L.direction == 0 ? 4 : 1); ++k)
+            if (!aligned(L.out[k], 16) || (L.nb > 1 && L.out_bstride[k] % 4 != 0)) return false;
+    }
     const int H = wl_host_program(L.prog).halo;
-    return wlfast::plan_tiles(L, H, R, NW).ok;
+    return wlfast::plan_tiles(L, H, R, NW, CPT).ok;
 }
 
 cudaError_t wl_launch_fast(const WlLevel& L, cudaStream_t stream) {
     if (!wl_fast_supported(L)) return cudaErrorNotSupported;
-    int R, NW;
-    geometry(L, &R, &NW);
+    int R, NW, CPT;
+    geometry(L, &R, &NW, &CPT);
     const int H = wl_host_program(L.prog).halo;
-    const wlfast::Plan plan = wlfast::plan_tiles(L, H, R, NW);
+    const wlfast::Plan plan = wlfast::plan_tiles(L, H, R, NW, CPT);
     cudaError_t e;
     if (L.wavelet == 0)
         e = L.direction == 0 ? wl_fast_cdf53_fwd(L.scheme, L, plan, stream)

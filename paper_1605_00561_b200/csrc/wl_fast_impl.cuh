@@ -48,8 +48,13 @@ namespace wlfast {
 #define WL_XCH_MBAR 0
 #endif
 
-constexpr int CPT = 2;   // component cells per lane per row
-constexpr int TWC = 64;  // compute-region width in cells (32 lanes x CPT)
+// CPT = component cells per lane per row (2 or 4); the compute region is
+// 32 * CPT cells wide. CPT = 4 stores one aligned float4 per lane and plane
+// and keeps tile boundaries on 32-byte sectors.
+// Horizontal halo of the stored columns: CPT = 2 uses the program's reach H;
+// CPT = 4 drops whole lanes (HX = 4 cells, lanes 0 and 31).
+template <int CPT, int H>
+constexpr int halo_x() { return CPT == 4 ? 4 : H; }
 
 template <class F, int... I>
 __device__ __forceinline__ void sfor_impl(F&& f, std::integer_sequence<int, I...>) {
@@ -121,6 +126,28 @@ __device__ __forceinline__ void mbar_wait_backoff(uint64_t* b, unsigned parity) 
         ns = ns < 256 ? 2 * ns : 256;
     }
 }
+// Producer wait, variant: try_wait with a suspend-time hint parks the thread
+// in hardware until the phase completes (no polling instructions).
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* b, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WL_WAIT_S:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+        "@!p bra WL_WAIT_S;\n}" ::"r"(smem_u32(b)),
+        "r"(parity), "r"(1000000u)
+        : "memory");
+}
+#ifndef WL_PROD_SLEEP
+#define WL_PROD_SLEEP 0
+#endif
+// Forward input tile as WL_FWD_SPLIT TMA boxes of 2*kRows/WL_FWD_SPLIT rows.
+#ifndef WL_FWD_SPLIT
+#define WL_FWD_SPLIT 1
+#endif
+#ifndef WL_STORE_PAIRS
+#define WL_STORE_PAIRS 0
+#endif
+
 __device__ __forceinline__ void named_sync(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
@@ -143,18 +170,21 @@ struct FastArgs {
     int ylo, yhi;        // stored cell rows [ylo, yhi); out[] addresses row ylo
 };
 
-template <int R, int NW>
+template <int R, int NW, int CPT>
 struct Geometry {
+    static constexpr int TWC = 32 * CPT;                     // compute-region width in cells
     static constexpr int kRows = NW * R + 2;                 // cell rows per stage incl. ghosts
     static constexpr int kStageFloats = 4 * TWC * kRows;     // == 2*TWC px * 2*kRows px
     static constexpr int kStageBytes = kStageFloats * 4;
     static constexpr int kXchFloats = 2 * NW * 2 * 32 * CPT * 4;
     static constexpr size_t kSmemBytes =
         2 * (size_t)kStageBytes + (size_t)kXchFloats * 4 + 64;
+    // CTAs per SM the shared memory allows (228 KB per SM, 1 KB reserved per CTA)
+    static constexpr int kMinBlocks = 2 * (kSmemBytes + 1024) <= 233472 ? 2 : 1;
 };
 
 // Neighbour accessor for the cell at (row RR, column CC) of the lane's block.
-template <int R, int RR, int CC>
+template <int R, int CPT, int RR, int CC>
 struct Acc {
     const float (&v)[R][CPT][4];
     const float (&gu)[CPT][4];
@@ -188,13 +218,15 @@ __host__ __device__ constexpr bool uses_dr(unsigned long long m, int c, int dr) 
     return uses(m, c, dr, -1) || uses(m, c, dr, 0) || uses(m, c, dr, 1);
 }
 
-template <class P, int DIR, int R, int NW>
-__global__ void __launch_bounds__((NW + 1) * 32, 2)
+template <class P, int DIR, int R, int NW, int CPT>
+__global__ void __launch_bounds__((NW + 1) * 32, (Geometry<R, NW, CPT>::kMinBlocks))
     fast_kernel(const __grid_constant__ CUtensorMap m0, const __grid_constant__ CUtensorMap m1,
                 const __grid_constant__ CUtensorMap m2, const __grid_constant__ CUtensorMap m3,
                 const FastArgs a) {
-    using G = Geometry<R, NW>;
+    using G = Geometry<R, NW, CPT>;
     constexpr int H = P::kHalo;
+    constexpr int TWC = G::TWC;
+    constexpr int HX = halo_x<CPT, H>();
     extern __shared__ __align__(128) unsigned char smem_raw[];
     float* stage = reinterpret_cast<float*>(smem_raw);
     float* xch = stage + 2 * G::kStageFloats;
@@ -219,16 +251,26 @@ __global__ void __launch_bounds__((NW + 1) * 32, 2)
         if (lane == 0) {
             for (int i = 0, t = blockIdx.x; t < a.ntiles; t += gridDim.x, ++i) {
                 const int s = i & 1;
-                if (i >= 2) mbar_wait_backoff(&empty[s], ((i >> 1) - 1) & 1);
+                if (i >= 2) {
+#if WL_PROD_SLEEP
+                    mbar_wait_sleep(&empty[s], ((i >> 1) - 1) & 1);
+#else
+                    mbar_wait_backoff(&empty[s], ((i >> 1) - 1) & 1);
+#endif
+                }
                 const int b = t / a.ntiles_img, tt = t - b * a.ntiles_img;
                 const int tyi = tt / a.tiles_x;
                 const int ty = tyi + a.ty0, tx = tt - tyi * a.tiles_x + a.tx0;
-                const int cx = a.X0 + tx * a.TW - H;      // first compute cell column
+                const int cx = a.X0 + tx * a.TW - HX;     // first compute cell column
                 const int cy = a.Y0 + ty * a.TH - H - 1;  // ghost row above the region
                 float* dst = stage + s * G::kStageFloats;
                 mbar_expect_tx(&full[s], G::kStageBytes);
                 if (DIR == 0) {
-                    tma_load_3d(dst, &m0, &full[s], 2 * cx, 2 * cy, b);
+                    constexpr int kSplitRows = 2 * G::kRows / WL_FWD_SPLIT;
+#pragma unroll
+                    for (int q = 0; q < WL_FWD_SPLIT; ++q)
+                        tma_load_3d(dst + q * kSplitRows * 2 * TWC, &m0, &full[s], 2 * cx,
+                                    2 * cy + q * kSplitRows, b);
                 } else {
                     constexpr int plane = TWC * G::kRows;
                     tma_load_3d(dst, &m0, &full[s], cx, cy, b);
@@ -252,7 +294,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 2)
         const int b = t / a.ntiles_img, tt = t - b * a.ntiles_img;
         const int tyi = tt / a.tiles_x;
         const int ty = tyi + a.ty0, tx = tt - tyi * a.tiles_x + a.tx0;
-        const int cx = a.X0 + tx * a.TW - H;      // first compute cell column
+        const int cx = a.X0 + tx * a.TW - HX;     // first compute cell column
         const int cy = a.Y0 + ty * a.TH - H - 1;  // ghost row above the region
         // Periodic border tile (only when the plan covers the whole image):
         // its cells are loaded with wrapped coordinates straight from global
@@ -287,19 +329,29 @@ __global__ void __launch_bounds__((NW + 1) * 32, 2)
                     }
                 }
             } else if (DIR == 0) {
-                const float* p0 = st + (2 * q) * (2 * TWC) + 4 * lane;
-                const float4 e = *reinterpret_cast<const float4*>(p0);
-                const float4 o = *reinterpret_cast<const float4*>(p0 + 2 * TWC);
-                dst[0][0] = e.x; dst[0][1] = e.y; dst[0][2] = o.x; dst[0][3] = o.y;
-                dst[1][0] = e.z; dst[1][1] = e.w; dst[1][2] = o.z; dst[1][3] = o.w;
+                // pixel rows 2q (LL HL LL HL ...) and 2q+1 (LH HH ...)
+                const float* p0 = st + (2 * q) * (2 * TWC) + 2 * CPT * lane;
+#pragma unroll
+                for (int jj = 0; jj < CPT / 2; ++jj) {
+                    const float4 e = *reinterpret_cast<const float4*>(p0 + 4 * jj);
+                    const float4 o = *reinterpret_cast<const float4*>(p0 + 2 * TWC + 4 * jj);
+                    dst[2 * jj][0] = e.x; dst[2 * jj][1] = e.y; dst[2 * jj][2] = o.x; dst[2 * jj][3] = o.y;
+                    dst[2 * jj + 1][0] = e.z; dst[2 * jj + 1][1] = e.w;
+                    dst[2 * jj + 1][2] = o.z; dst[2 * jj + 1][3] = o.w;
+                }
             } else {
                 constexpr int plane = TWC * G::kRows;
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
-                    const float2 p =
-                        *reinterpret_cast<const float2*>(st + c * plane + q * TWC + 2 * lane);
-                    dst[0][c] = p.x;
-                    dst[1][c] = p.y;
+                    const float* p = st + c * plane + q * TWC + CPT * lane;
+                    if constexpr (CPT == 4) {
+                        const float4 u = *reinterpret_cast<const float4*>(p);
+                        dst[0][c] = u.x; dst[1][c] = u.y; dst[2][c] = u.z; dst[3][c] = u.w;
+                    } else {
+                        const float2 u = *reinterpret_cast<const float2*>(p);
+                        dst[0][c] = u.x;
+                        dst[1][c] = u.y;
+                    }
                 }
             }
         };
@@ -376,7 +428,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 2)
             auto row = [&](auto r_) {
                 sfor<CPT>([&](auto c_) {
                     constexpr int RR = decltype(r_)::value, CC = decltype(c_)::value;
-                    Acc<R, RR, CC> acc{v, gu, gd, sl, sr};
+                    Acc<R, CPT, RR, CC> acc{v, gu, gd, sl, sr};
                     P::template nbr<E>(acc, o[RR][CC]);
                 });
             };
@@ -431,13 +483,6 @@ __global__ void __launch_bounds__((NW + 1) * 32, 2)
         // ---------------- store ----------------
         const int gy0 = cy + 1 + warp * R;  // global cell row of v[0]
         const int gx = cx + CPT * lane;     // global cell col of column 0
-        // output columns of this tile, clipped to the image (partial tiles)
-        const bool c0 = CPT * lane >= H && CPT * lane < H + a.TW && gx >= 0 && gx < a.qw;
-        const bool c1 =
-            CPT * lane + 1 >= H && CPT * lane + 1 < H + a.TW && gx + 1 >= 0 && gx + 1 < a.qw;
-        // Branch-free, predicated stores: both cells (vector store) / only
-        // the left / only the right cell. Row validity is warp-uniform.
-        const bool both = c0 && c1, only0 = c0 && !c1, only1 = c1 && !c0;
         if (DIR == 0 && a.scaling) {  // scale_planes (transform.cpp:154-159)
 #pragma unroll
             for (int r = 0; r < R; ++r)
@@ -454,6 +499,48 @@ __global__ void __launch_bounds__((NW + 1) * 32, 2)
 #pragma unroll
         for (int k = 0; k < (DIR == 0 ? 4 : 1); ++k) pk[k] = a.out[k] + b * a.out_bstride[k] + off0;
         const long step = DIR == 0 ? a.out_pitch : 2 * a.out_pitch;
+        if constexpr (CPT == 4) {
+            // Whole-lane halo (lanes 0 and 31): a lane stores its 4 cells as
+            // one aligned float4 per plane (qw = 0 mod 4, cx = 0 mod 4), or
+            // nothing. Row validity is warp-uniform.
+            const bool c_ok = lane >= HX / 4 && lane < 32 - HX / 4 && gx >= 0 && gx < a.qw;
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const int qr = warp * R + r;
+                const int gy = gy0 + r;
+                const bool ok = c_ok && qr >= H && qr < H + a.TH && gy >= a.ylo && gy < a.yhi;
+                if (DIR == 0) {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        if (ok)
+                            *reinterpret_cast<float4*>(pk[k] + r * step) =
+                                make_float4(v[r][0][k], v[r][1][k], v[r][2][k], v[r][3][k]);
+                } else {
+                    float* p0 = pk[0] + r * step;
+                    float* p1 = p0 + a.out_pitch;
+                    if (ok) {
+                        *reinterpret_cast<float4*>(p0) =
+                            make_float4(v[r][0][0], v[r][0][1], v[r][1][0], v[r][1][1]);
+                        *reinterpret_cast<float4*>(p0 + 4) =
+                            make_float4(v[r][2][0], v[r][2][1], v[r][3][0], v[r][3][1]);
+                        *reinterpret_cast<float4*>(p1) =
+                            make_float4(v[r][0][2], v[r][0][3], v[r][1][2], v[r][1][3]);
+                        *reinterpret_cast<float4*>(p1 + 4) =
+                            make_float4(v[r][2][2], v[r][2][3], v[r][3][2], v[r][3][3]);
+                    }
+                }
+            }
+        } else {
+        // output columns of this tile, clipped to the image (partial tiles)
+        const bool c0 = CPT * lane >= H && CPT * lane < H + a.TW && gx >= 0 && gx < a.qw;
+        const bool c1 =
+            CPT * lane + 1 >= H && CPT * lane + 1 < H + a.TW && gx + 1 >= 0 && gx + 1 < a.qw;
+        // Branch-free, predicated stores: both cells (vector store) / only
+        // the left / only the right cell. Row validity is warp-uniform.
+        // With an even halo a lane's two cells are both stored or both halo
+        // (only the "both" store exists); odd halos also need single cells.
+        constexpr bool kPairs = WL_STORE_PAIRS && (H % 2 == 0);
+        const bool both = c0 && c1, only0 = !kPairs && c0 && !c1, only1 = !kPairs && c1 && !c0;
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             const int qr = warp * R + r;
@@ -487,6 +574,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 2)
                 }
             }
         }
+        }  // CPT == 2
     }
 }
 
@@ -503,30 +591,61 @@ bool make_map(CUtensorMap* m, const float* base, int w, int h, long pitch, int n
               int box_w, int box_h);
 
 // Launch configuration per wavelet: (R, NW).
-template <int WAVELET>
+template <int WAVELET, int DIR>
 struct Config;
 // Tile geometry per wavelet, tuned on B200 at 16384^2 (fwd+inv pairs, see
 // profiles/tuning_r01.md): cdf53 R=3 x NW=8 (3 CTAs/SM, 27 warps),
 // cdf97 R=8 x NW=4 (deeper register rows, fewer exchanges per row).
-#ifndef WL_R53
-#define WL_R53 3
+// Geometry per (wavelet, direction): R rows per warp, NW compute warps, CPT
+// cells per lane. Tuned on B200 at 16384^2 (profiles/tuning_r01*.txt):
+// forwards use CPT = 4 (aligned float4 plane stores, sector-aligned tile
+// boundaries), inverses CPT = 2 (their interleaved float4 image rows are
+// already wide).
+#ifndef WL_CPT_FWD
+#define WL_CPT_FWD 4
 #endif
-#ifndef WL_NW53
-#define WL_NW53 8
+#ifndef WL_CPT_INV
+#define WL_CPT_INV 2
 #endif
-#ifndef WL_R97
-#define WL_R97 8
+#ifndef WL_R53F
+#define WL_R53F 3
 #endif
-#ifndef WL_NW97
-#define WL_NW97 4
+#ifndef WL_NW53F
+#define WL_NW53F 8
+#endif
+#ifndef WL_R97F
+#define WL_R97F 4
+#endif
+#ifndef WL_NW97F
+#define WL_NW97F 8
+#endif
+#ifndef WL_R53I
+#define WL_R53I 3
+#endif
+#ifndef WL_NW53I
+#define WL_NW53I 8
+#endif
+#ifndef WL_R97I
+#define WL_R97I 8
+#endif
+#ifndef WL_NW97I
+#define WL_NW97I 4
 #endif
 template <>
-struct Config<0> {  // cdf53, halo 1
-    static constexpr int R = WL_R53, NW = WL_NW53;
+struct Config<0, 0> {  // cdf53 forward, halo 1
+    static constexpr int R = WL_R53F, NW = WL_NW53F, CPT = WL_CPT_FWD;
 };
 template <>
-struct Config<1> {  // cdf97, halo 2
-    static constexpr int R = WL_R97, NW = WL_NW97;
+struct Config<0, 1> {  // cdf53 inverse
+    static constexpr int R = WL_R53I, NW = WL_NW53I, CPT = WL_CPT_INV;
+};
+template <>
+struct Config<1, 0> {  // cdf97 forward, halo 2
+    static constexpr int R = WL_R97F, NW = WL_NW97F, CPT = WL_CPT_FWD;
+};
+template <>
+struct Config<1, 1> {  // cdf97 inverse
+    static constexpr int R = WL_R97I, NW = WL_NW97I, CPT = WL_CPT_INV;
 };
 
 struct Plan {
@@ -544,38 +663,47 @@ struct Plan {
 //    [ylo, yhi) only; the rows around them are halo rows physically present
 //    in the buffer (ylo >= H + 1 and yhi <= qh - H - 1 keep every stored
 //    cell's dependency cone and the tiles' ghost rows inside the buffer).
-inline Plan plan_tiles(const WlLevel& L, int H, int R, int NW) {
+inline Plan plan_tiles(const WlLevel& L, int H, int R, int NW, int CPT) {
     Plan p{};
     const int nb = L.nb > 1 ? L.nb : 1;
     p.args.ylo = 0;
     p.args.yhi = L.qh;
+    const int TWC = 32 * CPT;
     // TMA requires the innermost box start to be 16-byte aligned: the inverse
-    // boxes start at cell column X0 - H + tx*TW of a float32 plane, so TW is
+    // boxes start at cell column X0 - HX + tx*TW of a float32 plane, so TW is
     // rounded down to a multiple of 4 there (the forward starts at pixel
     // column 2*(...) and 2*(64 - 2H) is a multiple of 4 for H = 1, 2).
-    const int TW = L.direction == 0 ? TWC - 2 * H : ((TWC - 2 * H) & ~3);
+    // CPT = 4: HX = 4, TW = 120; tile column 0 starts its compute region at
+    // cell -4 (X0 = 0) so every tile's stored columns start at 120*tx.
+    const int HX = CPT == 4 ? 4 : H;
+    const int TW = CPT == 4 ? TWC - 2 * HX
+                            : (L.direction == 0 ? TWC - 2 * H : ((TWC - 2 * H) & ~3));
     const int TH = NW * R - 2 * H;
-    const int X0 = H, Y0 = H + 1;
+    const bool wide = CPT == 4;
+    const int X0 = wide ? (L.boundary == 0 || L.yhi > 0 ? 0 : HX) : H, Y0 = H + 1;
+    const int tx0 = wide ? 0 : -1;  // periodic plans
     int tx, ty;
     int y0 = Y0;
     if (L.yhi > 0) {
         if (L.boundary != 0 || L.ylo < H + 1 || L.yhi > L.qh - H - 1 || L.yhi <= L.ylo)
             return p;  // ok = false
-        tx = (L.qw - X0 > 0 ? (L.qw - X0 + TW - 1) / TW : 0) + 1;
+        tx = (L.qw - X0 > 0 ? (L.qw - X0 + TW - 1) / TW : 0) - tx0;
         ty = (L.yhi - L.ylo + TH - 1) / TH;
         y0 = L.ylo;
-        p.args.tx0 = -1;
+        p.args.tx0 = tx0;
         p.args.ty0 = 0;
         p.args.wrap = 1;
         p.args.ylo = L.ylo;
         p.args.yhi = L.yhi;
     } else if (L.boundary == 0) {
-        tx = (L.qw - X0 > 0 ? (L.qw - X0 + TW - 1) / TW : 0) + 1;
+        tx = (L.qw - X0 > 0 ? (L.qw - X0 + TW - 1) / TW : 0) - tx0;
         ty = (L.qh - Y0 > 0 ? (L.qh - Y0 + TH - 1) / TH : 0) + 1;
-        p.args.tx0 = p.args.ty0 = -1;
+        p.args.tx0 = tx0;
+        p.args.ty0 = -1;
         p.args.wrap = 1;
     } else {
-        tx = L.qw >= TWC ? (L.qw - TWC) / TW + 1 : 0;
+        const int c0 = X0 - HX;  // first compute column of tile 0 (>= 0)
+        tx = L.qw - c0 >= TWC ? (L.qw - c0 - TWC) / TW + 1 : 0;
         const int span = L.qh - (Y0 - H - 1);  // rows available from the first ghost row
         ty = span >= NW * R + 2 ? (span - (NW * R + 2)) / TH + 1 : 0;
         p.args.tx0 = p.args.ty0 = 0;
@@ -595,9 +723,10 @@ inline Plan plan_tiles(const WlLevel& L, int H, int R, int NW) {
     return p;
 }
 
-template <class P, int DIR, int R, int NW>
+template <class P, int DIR, int R, int NW, int CPT>
 cudaError_t launch(const WlLevel& L, const Plan& plan, cudaStream_t stream) {
-    using G = Geometry<R, NW>;
+    using G = Geometry<R, NW, CPT>;
+    constexpr int TWC = G::TWC;
     CUtensorMap maps[4];
     FastArgs a = plan.args;
     const int nb = L.nb > 1 ? L.nb : 1;
@@ -606,8 +735,9 @@ cudaError_t launch(const WlLevel& L, const Plan& plan, cudaStream_t stream) {
         a.out_bstride[k] = nb > 1 ? L.out_bstride[k] : 0;
     }
     if (DIR == 0) {
+        static_assert((2 * G::kRows) % WL_FWD_SPLIT == 0, "split must divide the tile rows");
         if (!make_map(&maps[0], L.in[0], 2 * L.qw, 2 * L.qh, L.in_pitch, nb, a.in_bstride[0],
-                      2 * TWC, 2 * G::kRows))
+                      2 * TWC, 2 * G::kRows / WL_FWD_SPLIT))
             return cudaErrorInvalidValue;
         maps[1] = maps[2] = maps[3] = maps[0];
         for (int k = 0; k < 4; ++k) a.out[k] = L.out[k];
@@ -624,7 +754,7 @@ cudaError_t launch(const WlLevel& L, const Plan& plan, cudaStream_t stream) {
     a.out_pitch = L.out_pitch;
     a.scaling = L.scaling && wl_host_program(L.prog).has_scale;
     a.scale = wl_host_program(L.prog).scale;
-    auto kern = fast_kernel<P, DIR, R, NW>;
+    auto kern = fast_kernel<P, DIR, R, NW, CPT>;
     static int max_blocks[64] = {};
     int dev = 0;
     cudaGetDevice(&dev);
