@@ -144,6 +144,12 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* b, unsigned parity) {
 #ifndef WL_FWD_SPLIT
 #define WL_FWD_SPLIT 1
 #endif
+#ifndef WL_LDS_SWIZZLE
+#define WL_LDS_SWIZZLE 1
+#endif
+#ifndef WL_WRAP_MOD_INV
+#define WL_WRAP_MOD_INV 0
+#endif
 #ifndef WL_STORE_PAIRS
 #define WL_STORE_PAIRS 0
 #endif
@@ -309,19 +315,29 @@ __global__ void __launch_bounds__((NW + 1) * 32, (Geometry<R, NW, CPT>::kMinBloc
         auto load_row = [&](int q, float (&dst)[CPT][4]) {
             // q: cell row in the stage (0 = ghost row above the region)
             if (wrap_tile) {
-                int ry = (cy + q) % a.qh;
-                ry += ry < 0 ? a.qh : 0;
+                // periodic wrap: one conditional add/subtract unless the image
+                // is smaller than a tile (then the general modulo)
+                const bool small = WL_WRAP_MOD_INV && DIR == 1 || a.qw < TWC || a.qh < G::kRows;
+                auto wrapi = [small](int i, int n) {
+                    if (small) {
+                        i %= n;
+                        return i < 0 ? i + n : i;
+                    }
+                    return i < 0 ? i + n : (i >= n ? i - n : i);
+                };
+                const int ry = wrapi(cy + q, a.qh);
 #pragma unroll
                 for (int j = 0; j < CPT; ++j) {
-                    int rx = (cx + CPT * lane + j) % a.qw;
-                    rx += rx < 0 ? a.qw : 0;
+                    const int rx = wrapi(cx + CPT * lane + j, a.qw);
                     if (DIR == 0) {
                         const float* p =
                             a.in[0] + b * a.in_bstride[0] + (long)(2 * ry) * a.in_pitch + 2 * rx;
-                        dst[j][0] = p[0];
-                        dst[j][1] = p[1];
-                        dst[j][2] = p[a.in_pitch];
-                        dst[j][3] = p[a.in_pitch + 1];
+                        const float2 u0 = *reinterpret_cast<const float2*>(p);
+                        const float2 u1 = *reinterpret_cast<const float2*>(p + a.in_pitch);
+                        dst[j][0] = u0.x;
+                        dst[j][1] = u0.y;
+                        dst[j][2] = u1.x;
+                        dst[j][3] = u1.y;
                     } else {
 #pragma unroll
                         for (int c = 0; c < 4; ++c)
@@ -331,13 +347,37 @@ __global__ void __launch_bounds__((NW + 1) * 32, (Geometry<R, NW, CPT>::kMinBloc
             } else if (DIR == 0) {
                 // pixel rows 2q (LL HL LL HL ...) and 2q+1 (LH HH ...)
                 const float* p0 = st + (2 * q) * (2 * TWC) + 2 * CPT * lane;
+                float4 e[CPT / 2], o[CPT / 2];
+                if constexpr (CPT == 4) {
+                    // lanes 32 B apart: read the two 16-B halves in an order
+                    // swizzled by lane group so every 8-lane phase covers all
+                    // 32 banks (no 2-way conflict), then undo the swap
+#if WL_LDS_SWIZZLE
+                    const int sw = (lane >> 2) & 1;
+                    const float4 e0 = *reinterpret_cast<const float4*>(p0 + 4 * sw);
+                    const float4 e1 = *reinterpret_cast<const float4*>(p0 + 4 * (sw ^ 1));
+                    const float4 o0 = *reinterpret_cast<const float4*>(p0 + 2 * TWC + 4 * sw);
+                    const float4 o1 = *reinterpret_cast<const float4*>(p0 + 2 * TWC + 4 * (sw ^ 1));
+                    e[0] = sw ? e1 : e0;
+                    e[1] = sw ? e0 : e1;
+                    o[0] = sw ? o1 : o0;
+                    o[1] = sw ? o0 : o1;
+#else
+                    e[0] = *reinterpret_cast<const float4*>(p0);
+                    e[1] = *reinterpret_cast<const float4*>(p0 + 4);
+                    o[0] = *reinterpret_cast<const float4*>(p0 + 2 * TWC);
+                    o[1] = *reinterpret_cast<const float4*>(p0 + 2 * TWC + 4);
+#endif
+                } else {
+                    e[0] = *reinterpret_cast<const float4*>(p0);
+                    o[0] = *reinterpret_cast<const float4*>(p0 + 2 * TWC);
+                }
 #pragma unroll
                 for (int jj = 0; jj < CPT / 2; ++jj) {
-                    const float4 e = *reinterpret_cast<const float4*>(p0 + 4 * jj);
-                    const float4 o = *reinterpret_cast<const float4*>(p0 + 2 * TWC + 4 * jj);
-                    dst[2 * jj][0] = e.x; dst[2 * jj][1] = e.y; dst[2 * jj][2] = o.x; dst[2 * jj][3] = o.y;
-                    dst[2 * jj + 1][0] = e.z; dst[2 * jj + 1][1] = e.w;
-                    dst[2 * jj + 1][2] = o.z; dst[2 * jj + 1][3] = o.w;
+                    dst[2 * jj][0] = e[jj].x; dst[2 * jj][1] = e[jj].y;
+                    dst[2 * jj][2] = o[jj].x; dst[2 * jj][3] = o[jj].y;
+                    dst[2 * jj + 1][0] = e[jj].z; dst[2 * jj + 1][1] = e[jj].w;
+                    dst[2 * jj + 1][2] = o[jj].z; dst[2 * jj + 1][3] = o[jj].w;
                 }
             } else {
                 constexpr int plane = TWC * G::kRows;
