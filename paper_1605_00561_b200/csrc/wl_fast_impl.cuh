@@ -148,7 +148,7 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* b, unsigned parity) {
 #define WL_LDS_SWIZZLE 1
 #endif
 #ifndef WL_WRAP_MOD_INV
-#define WL_WRAP_MOD_INV 0
+#define WL_WRAP_MOD_INV 1
 #endif
 #ifndef WL_STORE_PAIRS
 #define WL_STORE_PAIRS 0
