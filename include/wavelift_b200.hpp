@@ -21,6 +21,7 @@
 #include <optional>
 #include <stdexcept>
 #include <string>
+#include <algorithm>
 #include <vector>
 
 #include "wl_dwt.h"
@@ -213,21 +214,21 @@ inline Image polyphase_merge(const QuadGrid& q) {
     return img;
 }
 
-// transform.cpp:163-176
+// transform.cpp:163-176. Host in / host out through wl_dwt2_forward_host
+// (row-chunk pipeline: PCIe both ways overlaps the kernels).
 inline QuadGrid forward(const Image& img, const Scheme& s, BoundaryMode b, bool apply_scaling) {
     if (img.width <= 0 || img.height <= 0 || img.width % 2 || img.height % 2)
         throw std::invalid_argument("forward requires even positive dimensions");
     const int qw = img.width / 2, qh = img.height / 2;
     const std::size_t n = static_cast<std::size_t>(qw) * qh;
-    detail::DevBuf in(img.samples.size()), out(4 * n);
-    in.upload(img.samples.data(), img.samples.size());
-    detail::check(wl_dwt2_forward(in.p, img.width, img.height, img.width, s.wavelet.id,
-                                  static_cast<int>(s.kind), detail::boundary_id(b),
-                                  apply_scaling ? 1 : 0, out.p, out.p + n, out.p + 2 * n,
-                                  out.p + 3 * n, qw, nullptr));
-    detail::cuda(cudaDeviceSynchronize(), "forward");
+    std::vector<float> in(img.samples.begin(), img.samples.end()), out(4 * n);
+    detail::check(wl_dwt2_forward_host(in.data(), img.width, img.height, img.width, s.wavelet.id,
+                                       static_cast<int>(s.kind), detail::boundary_id(b),
+                                       apply_scaling ? 1 : 0, out.data(), out.data() + n,
+                                       out.data() + 2 * n, out.data() + 3 * n, qw));
     QuadGrid q(qw, qh);
-    for (int c = 0; c < 4; ++c) out.download(q.planes[c].data(), n, c * n);
+    for (int c = 0; c < 4; ++c)
+        q.planes[c].assign(out.begin() + c * n, out.begin() + (c + 1) * n);
     return q;
 }
 
@@ -238,14 +239,14 @@ inline Image inverse(const QuadGrid& q, const WaveletSpec& w, BoundaryMode b, bo
     const std::size_t n = static_cast<std::size_t>(q.w) * q.h;
     for (const auto& p : q.planes)
         if (p.size() != n) throw std::invalid_argument("quad grid plane size mismatch");
-    detail::DevBuf in(4 * n), out(4 * n);
-    for (int c = 0; c < 4; ++c) in.upload(q.planes[c].data(), n, c * n);
-    detail::check(wl_dwt2_inverse(in.p, in.p + n, in.p + 2 * n, in.p + 3 * n, q.w, q.h, q.w, w.id,
-                                  static_cast<int>(kind), detail::boundary_id(b),
-                                  undo_scaling ? 1 : 0, out.p, 2 * q.w, nullptr));
-    detail::cuda(cudaDeviceSynchronize(), "inverse");
+    std::vector<float> in(4 * n), out(4 * n);
+    for (int c = 0; c < 4; ++c) std::copy(q.planes[c].begin(), q.planes[c].end(), in.begin() + c * n);
+    detail::check(wl_dwt2_inverse_host(in.data(), in.data() + n, in.data() + 2 * n,
+                                       in.data() + 3 * n, q.w, q.h, q.w, w.id,
+                                       static_cast<int>(kind), detail::boundary_id(b),
+                                       undo_scaling ? 1 : 0, out.data(), 2 * q.w));
     Image img(2 * q.w, 2 * q.h);
-    out.download(img.samples.data(), img.samples.size());
+    img.samples.assign(out.begin(), out.end());
     return img;
 }
 
