@@ -446,6 +446,11 @@ __global__ void __launch_bounds__((NW + 1) * 32, (Geometry<R, NW, CPT>::kMinBloc
 #if WL_XCH_MBAR
                 mbar_arrive(&xbar[xslot]);  // release: this lane's edge stores
 #else
+#ifdef WL_BREAK_BARRIER
+                // negative control (acceptance.cpp:283-296 / parsim break_barrier):
+                // drop the barrier of epoch WL_BREAK_BARRIER; racecheck must flag it
+                if constexpr (E != WL_BREAK_BARRIER)
+#endif
                 named_sync(1, NW * 32);  // the epoch's block barrier
 #endif
             }

@@ -1,0 +1,62 @@
+"""Barrier structure on real SASS (the reference checks it on its simulator,
+acceptance.cpp:236-254 / test_parsim.cpp:101-115): every fast-engine kernel
+contains exactly count_barriers(scheme) block barriers -- the initial
+data-availability barrier plus one per epoch after the first -- and the
+compile-time negative control WL_BREAK_BARRIER drops exactly one (racecheck
+flags the resulting hazard: test_gpu_race.py). CPU-only: cuobjdump on the
+built library."""
+import os
+import re
+import shutil
+import subprocess
+
+import pytest
+
+import paper_1605_00561_b200 as wl
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+CUOBJDUMP = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+
+
+def barrier_counts(lib_path):
+    out = subprocess.run([CUOBJDUMP, "-sass", lib_path], capture_output=True, text=True,
+                         check=True).stdout
+    counts, fn = {}, None
+    for line in out.splitlines():
+        m = re.search(r"Function : (\S+)", line)
+        if m:
+            fn = m.group(1)
+            km = re.search(r"fast_kernelI\d+P_(cdf\d+)_(\w+?)_(fwd|inv)", fn)
+            fn = km.groups() if km else None
+            if fn:
+                counts.setdefault(fn, 0)
+            continue
+        if fn and re.search(r"\bBAR\.(SYNC|RED|ARV)", line):
+            counts[fn] += 1
+    return counts
+
+
+@pytest.mark.skipif(not os.path.exists(CUOBJDUMP), reason="cuobjdump not available")
+def test_sass_barriers_equal_count_barriers():
+    counts = barrier_counts(wl.LIB_PATH)
+    assert len(counts) == 2 * 9 * 2, sorted(counts)
+    for (w, s, d), n in counts.items():
+        want = wl.build_scheme(s, w).info(0 if d == "fwd" else 1)["barriers"]
+        assert n == want, (w, s, d, n, want)
+
+
+def build_broken(epoch=1):
+    env = dict(os.environ, WL_VARIANT=f"brk{epoch}", WL_DEFS=f"-DWL_BREAK_BARRIER={epoch}")
+    subprocess.run([os.sys.executable, "-m", "paper_1605_00561_b200._build"], cwd=ROOT, env=env,
+                   check=True, capture_output=True)
+    return os.path.join(ROOT, "paper_1605_00561_b200", f"libwavelift_b200_brk{epoch}.so")
+
+
+@pytest.mark.skipif(not os.path.exists(CUOBJDUMP), reason="cuobjdump not available")
+def test_broken_barrier_variant_drops_one_barrier():
+    lib = build_broken(1)
+    counts = barrier_counts(lib)
+    for (w, s, d), n in counts.items():
+        want = wl.build_scheme(s, w).info(0 if d == "fwd" else 1)["barriers"]
+        # epoch 1 exists only for schemes with >= 2 barriers
+        assert n == (want - 1 if want >= 2 else want), (w, s, d, n, want)
