@@ -13,8 +13,10 @@
 // (cudaHostRegister / cudaHostAlloc) for the copies to run asynchronously.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "../../include/wl_dwt.h"
 #include "wl_internal.h"
@@ -84,6 +86,15 @@ int cuda_err(cudaError_t e, const char* where) {
     return herr(WL_ERUNTIME, std::string(where) + ": " + cudaGetErrorString(e));
 }
 
+// Row-block copy: one linear DMA when both sides are dense, else 2-D.
+cudaError_t copy_rows(void* dst, long dpitch, const void* src, long spitch, int w, int rows,
+                      cudaMemcpyKind kind, cudaStream_t s) {
+    if (dpitch == w && spitch == w)
+        return cudaMemcpyAsync(dst, src, static_cast<size_t>(w) * rows * 4, kind, s);
+    return cudaMemcpy2DAsync(dst, dpitch * 4, src, spitch * 4, static_cast<size_t>(w) * 4, rows,
+                             kind, s);
+}
+
 // Copy host rows [r0, r1) of a periodic image (rows wrap mod h) into
 // consecutive device rows.
 cudaError_t rows_h2d(float* dst, long dpitch, const float* src, long spitch, int w, int h, int r0,
@@ -93,20 +104,61 @@ cudaError_t rows_h2d(float* dst, long dpitch, const float* src, long spitch, int
         int rr = r % h;
         rr += rr < 0 ? h : 0;
         const int n = (r1 - r) < (h - rr) ? (r1 - r) : (h - rr);
-        cudaError_t e = cudaMemcpy2DAsync(dst + static_cast<long>(r - r0) * dpitch, dpitch * 4,
-                                          src + static_cast<long>(rr) * spitch, spitch * 4, w * 4,
-                                          n, cudaMemcpyHostToDevice, s);
+        cudaError_t e = copy_rows(dst + static_cast<long>(r - r0) * dpitch, dpitch,
+                                  src + static_cast<long>(rr) * spitch, spitch, w, n,
+                                  cudaMemcpyHostToDevice, s);
         if (e != cudaSuccess) return e;
         r += n;
     }
     return cudaSuccess;
 }
 
+long chunk_bytes() {
+    static const long v = [] {
+        const char* e = getenv("WL_HOST_CHUNK_KB");  // tuning override
+        const long kb = e ? atol(e) : 0;
+        return kb > 0 ? kb * 1024 : static_cast<long>(kChunkBytes);
+    }();
+    return v;
+}
+
 int chunk_rows(long row_bytes, int total, int align) {
-    long r = static_cast<long>(kChunkBytes) / (row_bytes > 0 ? row_bytes : 1);
+    long r = chunk_bytes() / (row_bytes > 0 ? row_bytes : 1);
     r = r < 64 ? 64 : r;
     r -= r % align;
     return r >= total ? total : static_cast<int>(r);
+}
+
+// Chunk schedule over `total` rows: geometric ramp-up (R/8, R/4, R/2), steady
+// chunks of ~R, ramp-down at the end -- the first chunk's H2D and the last
+// chunk's D2H run without overlap, so they are kept small. Every chunk is a
+// multiple of `align` rows.
+std::vector<int> chunk_plan(int total, int R, int align) {
+    std::vector<int> ramp;
+    for (int r = R / 8; r < R; r *= 2) {
+        const int rr = r - r % align;
+        if (rr >= align) ramp.push_back(rr);
+    }
+    int rs = 0;
+    for (int r : ramp) rs += r;
+    std::vector<int> out;
+    if (total < 2 * rs + R) {  // too small to ramp: uniform chunks
+        for (int r0 = 0; r0 < total; r0 += R) out.push_back(R < total - r0 ? R : total - r0);
+        return out;
+    }
+    out = ramp;
+    const int mid = total - 2 * rs;
+    const int nmid = (mid + R - 1) / R;
+    int left = mid;
+    for (int i = 0; i < nmid; ++i) {
+        int c = left / (nmid - i);
+        c -= c % align;
+        if (i == nmid - 1) c = left;
+        out.push_back(c);
+        left -= c;
+    }
+    for (auto it = ramp.rbegin(); it != ramp.rend(); ++it) out.push_back(*it);
+    return out;
 }
 
 }  // namespace
@@ -152,12 +204,13 @@ int wl_dwt2_forward_host(const float* img, int w, int h, long img_pitch, int wav
     const size_t nin = static_cast<size_t>(w) * (R + 2 * halo);
     const size_t np = static_cast<size_t>(qw) * (R / 2);
     if (!g_ws.ensure(nin, 4 * np)) return herr(WL_ERUNTIME, "device workspace allocation failed");
-    int k = 0;
-    for (int r0 = 0; r0 < h; r0 += R, ++k) {
+    const std::vector<int> plan = chunk_plan(h, R, 2);
+    int r0 = 0;
+    for (size_t k = 0; k < plan.size(); r0 += plan[k], ++k) {
         const int s = k % kSlots;
         cudaStream_t st = g_ws.streams[s];
-        const int r1 = r0 + R < h ? r0 + R : h;
-        const int rows = r1 - r0;
+        const int rows = plan[k];
+        const int r1 = r0 + rows;
         cudaError_t e = rows_h2d(g_ws.in[s], w, img, img_pitch, w, h, r0 - halo, r1 + halo, st);
         if (e != cudaSuccess) return cuda_err(e, "H2D");
         float* o = g_ws.out[s];
@@ -167,9 +220,8 @@ int wl_dwt2_forward_host(const float* img, int w, int h, long img_pitch, int wav
                                             o + 2 * npc, o + 3 * npc, qw, st);
         if (r != WL_OK) return r;
         for (int c = 0; c < 4; ++c) {
-            e = cudaMemcpy2DAsync(hp[c] + static_cast<long>(r0 / 2) * plane_pitch,
-                                  plane_pitch * 4, o + c * npc, qw * 4, qw * 4, rows / 2,
-                                  cudaMemcpyDeviceToHost, st);
+            e = copy_rows(hp[c] + static_cast<long>(r0 / 2) * plane_pitch, plane_pitch,
+                          o + c * npc, qw, qw, rows / 2, cudaMemcpyDeviceToHost, st);
             if (e != cudaSuccess) return cuda_err(e, "D2H");
         }
     }
@@ -216,12 +268,13 @@ int wl_dwt2_inverse_host(const float* ll, const float* hl, const float* lh, cons
     const size_t npb = static_cast<size_t>(qw) * (R + 2 * halo);  // one plane buffer
     if (!g_ws.ensure(4 * npb, static_cast<size_t>(4) * qw * R))
         return herr(WL_ERUNTIME, "device workspace allocation failed");
-    int k = 0;
-    for (int q0 = 0; q0 < qh; q0 += R, ++k) {
+    const std::vector<int> plan = chunk_plan(qh, R, 1);
+    int q0 = 0;
+    for (size_t k = 0; k < plan.size(); q0 += plan[k], ++k) {
         const int s = k % kSlots;
         cudaStream_t st = g_ws.streams[s];
-        const int q1 = q0 + R < qh ? q0 + R : qh;
-        const int rows = q1 - q0;
+        const int rows = plan[k];
+        const int q1 = q0 + rows;
         const size_t pb = static_cast<size_t>(qw) * (rows + 2 * halo);
         for (int c = 0; c < 4; ++c) {
             cudaError_t e = rows_h2d(g_ws.in[s] + c * pb, qw, hp[c], plane_pitch, qw, qh,
@@ -233,9 +286,9 @@ int wl_dwt2_inverse_host(const float* ll, const float* hl, const float* lh, cons
                                             wavelet, scheme, undo_scaling, g_ws.out[s], 2 * qw,
                                             st);
         if (r != WL_OK) return r;
-        cudaError_t e = cudaMemcpy2DAsync(img + static_cast<long>(2 * q0) * img_pitch,
-                                          img_pitch * 4, g_ws.out[s], 2 * qw * 4, 2 * qw * 4,
-                                          2 * rows, cudaMemcpyDeviceToHost, st);
+        cudaError_t e = copy_rows(img + static_cast<long>(2 * q0) * img_pitch, img_pitch,
+                                  g_ws.out[s], 2 * qw, 2 * qw, 2 * rows, cudaMemcpyDeviceToHost,
+                                  st);
         if (e != cudaSuccess) return cuda_err(e, "D2H");
     }
     for (int s = 0; s < kSlots; ++s) {
