@@ -7,7 +7,7 @@ cudaError_t wl_fast_cdf97_inv(int scheme, const WlLevel& L, const wlfast::Plan& 
     switch (scheme) {
 #define WL_CASE(wi, si, d, P) \
     case si:                  \
-        return wlfast::launch<P, d, C::R, C::NW, C::CPT>(L, p, s);
+        return wlfast::launch<P, d, C::R, C::NW, C::CPT, C::NS>(L, p, s);
         WL_FAST_FOREACH_1_1(WL_CASE)
 #undef WL_CASE
         default:

@@ -2,7 +2,7 @@
 //
 // Persistent CTAs; warp-specialised:
 //   * 1 producer warp streams tiles HBM -> shared memory with TMA
-//     (cp.async.bulk.tensor.2d) into a 2-stage ring guarded by mbarriers
+//     (cp.async.bulk.tensor.3d) into an NS-stage ring guarded by mbarriers
 //     ("full": transaction-count barrier armed with the stage's bytes;
 //     "empty": one arrival per compute warp once it has copied its rows).
 //   * NW compute warps hold the tile in registers: warp w owns R rows of
@@ -40,6 +40,19 @@
 #include "wl_internal.h"
 
 namespace wlfast {
+
+// Producer wait on a released stage: 0 = test_wait + __nanosleep back-off
+// (cap WL_PROD_BACKOFF_NS), 1 = try_wait with a suspend hint, 2 = plain
+// try_wait loop (hardware-timed suspend).
+#ifndef WL_PROD_SLEEP
+#define WL_PROD_SLEEP 0
+#endif
+#ifndef WL_PROD_HINT_NS
+#define WL_PROD_HINT_NS 1000000u
+#endif
+#ifndef WL_PROD_BACKOFF_NS
+#define WL_PROD_BACKOFF_NS 256
+#endif
 
 // Edge exchange between compute warps: 0 = one bar.sync per epoch (default),
 // 1 = split-phase mbarrier (arrive after publishing, wait before the edge
@@ -123,7 +136,7 @@ __device__ __forceinline__ void mbar_wait_backoff(uint64_t* b, unsigned parity) 
     unsigned ns = 32;
     while (!mbar_test(b, parity)) {
         __nanosleep(ns);
-        ns = ns < 256 ? 2 * ns : 256;
+        ns = ns < WL_PROD_BACKOFF_NS ? 2 * ns : WL_PROD_BACKOFF_NS;
     }
 }
 // Producer wait, variant: try_wait with a suspend-time hint parks the thread
@@ -134,12 +147,9 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* b, unsigned parity) {
         "WL_WAIT_S:\n\t"
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
         "@!p bra WL_WAIT_S;\n}" ::"r"(smem_u32(b)),
-        "r"(parity), "r"(1000000u)
+        "r"(parity), "r"(WL_PROD_HINT_NS)
         : "memory");
 }
-#ifndef WL_PROD_SLEEP
-#define WL_PROD_SLEEP 0
-#endif
 // Forward input tile as WL_FWD_SPLIT TMA boxes of 2*kRows/WL_FWD_SPLIT rows.
 #ifndef WL_FWD_SPLIT
 #define WL_FWD_SPLIT 1
@@ -176,15 +186,16 @@ struct FastArgs {
     int ylo, yhi;        // stored cell rows [ylo, yhi); out[] addresses row ylo
 };
 
-template <int R, int NW, int CPT>
+template <int R, int NW, int CPT, int NS = 2>
 struct Geometry {
+    static constexpr int kStages = NS;                       // TMA ring depth
     static constexpr int TWC = 32 * CPT;                     // compute-region width in cells
     static constexpr int kRows = NW * R + 2;                 // cell rows per stage incl. ghosts
     static constexpr int kStageFloats = 4 * TWC * kRows;     // == 2*TWC px * 2*kRows px
     static constexpr int kStageBytes = kStageFloats * 4;
     static constexpr int kXchFloats = 2 * NW * 2 * 32 * CPT * 4;
     static constexpr size_t kSmemBytes =
-        2 * (size_t)kStageBytes + (size_t)kXchFloats * 4 + 64;
+        NS * (size_t)kStageBytes + (size_t)kXchFloats * 4 + 16 * NS;
     // CTAs per SM the shared memory allows (228 KB per SM, 1 KB reserved per CTA)
     static constexpr int kMinBlocks = 2 * (kSmemBytes + 1024) <= 233472 ? 2 : 1;
 };
@@ -224,30 +235,27 @@ __host__ __device__ constexpr bool uses_dr(unsigned long long m, int c, int dr) 
     return uses(m, c, dr, -1) || uses(m, c, dr, 0) || uses(m, c, dr, 1);
 }
 
-template <class P, int DIR, int R, int NW, int CPT>
-__global__ void __launch_bounds__((NW + 1) * 32, (Geometry<R, NW, CPT>::kMinBlocks))
+template <class P, int DIR, int R, int NW, int CPT, int NS>
+__global__ void __launch_bounds__((NW + 1) * 32, (Geometry<R, NW, CPT, NS>::kMinBlocks))
     fast_kernel(const __grid_constant__ CUtensorMap m0, const __grid_constant__ CUtensorMap m1,
                 const __grid_constant__ CUtensorMap m2, const __grid_constant__ CUtensorMap m3,
                 const FastArgs a) {
-    using G = Geometry<R, NW, CPT>;
+    using G = Geometry<R, NW, CPT, NS>;
     constexpr int H = P::kHalo;
     constexpr int TWC = G::TWC;
     constexpr int HX = halo_x<CPT, H>();
     extern __shared__ __align__(128) unsigned char smem_raw[];
     float* stage = reinterpret_cast<float*>(smem_raw);
-    float* xch = stage + 2 * G::kStageFloats;
+    float* xch = stage + NS * G::kStageFloats;
     uint64_t* full = reinterpret_cast<uint64_t*>(xch + G::kXchFloats);
-    uint64_t* empty = full + 2;
-    uint64_t* xbar = full + 4;  // split-phase edge-exchange barriers, one per slot
+    uint64_t* empty = full + NS;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
-        mbar_init(&full[0], 1);
-        mbar_init(&full[1], 1);
-        mbar_init(&empty[0], NW * 32);
-        mbar_init(&empty[1], NW * 32);
-        mbar_init(&xbar[0], NW * 32);
-        mbar_init(&xbar[1], NW * 32);
+        for (int k = 0; k < NS; ++k) {
+            mbar_init(&full[k], 1);
+            mbar_init(&empty[k], NW * 32);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -256,12 +264,15 @@ __global__ void __launch_bounds__((NW + 1) * 32, (Geometry<R, NW, CPT>::kMinBloc
         // ---------------- producer warp: TMA tile stream ----------------
         if (lane == 0) {
             for (int i = 0, t = blockIdx.x; t < a.ntiles; t += gridDim.x, ++i) {
-                const int s = i & 1;
-                if (i >= 2) {
-#if WL_PROD_SLEEP
-                    mbar_wait_sleep(&empty[s], ((i >> 1) - 1) & 1);
+                const int s = i % NS;
+                const unsigned use = i / NS;  // how often stage s was filled before
+                if (i >= NS) {
+#if WL_PROD_SLEEP == 1
+                    mbar_wait_sleep(&empty[s], (use - 1) & 1);
+#elif WL_PROD_SLEEP == 2
+                    mbar_wait(&empty[s], (use - 1) & 1);
 #else
-                    mbar_wait_backoff(&empty[s], ((i >> 1) - 1) & 1);
+                    mbar_wait_backoff(&empty[s], (use - 1) & 1);
 #endif
                 }
                 const int b = t / a.ntiles_img, tt = t - b * a.ntiles_img;
@@ -296,7 +307,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, (Geometry<R, NW, CPT>::kMinBloc
     unsigned xphase = 0;  // parity of the next phase to wait for, per slot (bit s)
 
     for (int i = 0, t = blockIdx.x; t < a.ntiles; t += gridDim.x, ++i) {
-        const int s = i & 1;
+        const int s = i % NS;
         const int b = t / a.ntiles_img, tt = t - b * a.ntiles_img;
         const int tyi = tt / a.tiles_x;
         const int ty = tyi + a.ty0, tx = tt - tyi * a.tiles_x + a.tx0;
@@ -307,7 +318,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, (Geometry<R, NW, CPT>::kMinBloc
         // memory -- load-time wrap is exact for the periodic extension.
         const bool wrap_tile =
             a.wrap && (cx < 0 || cy < 0 || cx + TWC > a.qw || cy + G::kRows > a.qh);
-        mbar_wait(&full[s], (i >> 1) & 1);
+        mbar_wait(&full[s], (i / NS) & 1);
         const float* st = stage + s * G::kStageFloats;
 
         // Load the warp's rows (+ one ghost row above and below) and split
@@ -424,6 +435,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, (Geometry<R, NW, CPT>::kMinBloc
             for (int r = 0; r < R; ++r) P::pre(v[r][c]);
         }
 
+#ifndef WL_DIAG_NO_COMPUTE
         sfor<P::kEpochs>([&](auto e_) {
             constexpr int E = decltype(e_)::value;
             constexpr unsigned long long U = P::kUse[E];
@@ -525,6 +537,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, (Geometry<R, NW, CPT>::kMinBloc
                 }
         });
 
+#endif  // WL_DIAG_NO_COMPUTE
         // ---------------- store ----------------
         const int gy0 = cy + 1 + warp * R;  // global cell row of v[0]
         const int gx = cx + CPT * lane;     // global cell col of column 0
@@ -553,7 +566,11 @@ __global__ void __launch_bounds__((NW + 1) * 32, (Geometry<R, NW, CPT>::kMinBloc
             for (int r = 0; r < R; ++r) {
                 const int qr = warp * R + r;
                 const int gy = gy0 + r;
+#ifdef WL_DIAG_NO_STORE
+                const bool ok = a.ylo == -777;  // diagnostic: compute only (never true, not DCE-able)
+#else
                 const bool ok = c_ok && qr >= H && qr < H + a.TH && gy >= a.ylo && gy < a.yhi;
+#endif
                 if (DIR == 0) {
 #pragma unroll
                     for (int k = 0; k < 4; ++k)
@@ -652,6 +669,18 @@ struct Config;
 #ifndef WL_CPT_INV
 #define WL_CPT_INV 2
 #endif
+#ifndef WL_NS53F
+#define WL_NS53F 3
+#endif
+#ifndef WL_NS53I
+#define WL_NS53I 2
+#endif
+#ifndef WL_NS97F
+#define WL_NS97F 2
+#endif
+#ifndef WL_NS97I
+#define WL_NS97I 2
+#endif
 #ifndef WL_R53F
 #define WL_R53F 3
 #endif
@@ -678,19 +707,19 @@ struct Config;
 #endif
 template <>
 struct Config<0, 0> {  // cdf53 forward, halo 1
-    static constexpr int R = WL_R53F, NW = WL_NW53F, CPT = WL_CPT_FWD;
+    static constexpr int R = WL_R53F, NW = WL_NW53F, CPT = WL_CPT_FWD, NS = WL_NS53F;
 };
 template <>
 struct Config<0, 1> {  // cdf53 inverse
-    static constexpr int R = WL_R53I, NW = WL_NW53I, CPT = WL_CPT_INV;
+    static constexpr int R = WL_R53I, NW = WL_NW53I, CPT = WL_CPT_INV, NS = WL_NS53I;
 };
 template <>
 struct Config<1, 0> {  // cdf97 forward, halo 2
-    static constexpr int R = WL_R97F, NW = WL_NW97F, CPT = WL_CPT_FWD;
+    static constexpr int R = WL_R97F, NW = WL_NW97F, CPT = WL_CPT_FWD, NS = WL_NS97F;
 };
 template <>
 struct Config<1, 1> {  // cdf97 inverse
-    static constexpr int R = WL_R97I, NW = WL_NW97I, CPT = WL_CPT_INV;
+    static constexpr int R = WL_R97I, NW = WL_NW97I, CPT = WL_CPT_INV, NS = WL_NS97I;
 };
 
 struct Plan {
@@ -768,9 +797,9 @@ inline Plan plan_tiles(const WlLevel& L, int H, int R, int NW, int CPT) {
     return p;
 }
 
-template <class P, int DIR, int R, int NW, int CPT>
+template <class P, int DIR, int R, int NW, int CPT, int NS>
 cudaError_t launch(const WlLevel& L, const Plan& plan, cudaStream_t stream) {
-    using G = Geometry<R, NW, CPT>;
+    using G = Geometry<R, NW, CPT, NS>;
     constexpr int TWC = G::TWC;
     CUtensorMap maps[4];
     FastArgs a = plan.args;
@@ -799,7 +828,7 @@ cudaError_t launch(const WlLevel& L, const Plan& plan, cudaStream_t stream) {
     a.out_pitch = L.out_pitch;
     a.scaling = L.scaling && wl_host_program(L.prog).has_scale;
     a.scale = wl_host_program(L.prog).scale;
-    auto kern = fast_kernel<P, DIR, R, NW, CPT>;
+    auto kern = fast_kernel<P, DIR, R, NW, CPT, NS>;
     static int max_blocks[64] = {};
     int dev = 0;
     cudaGetDevice(&dev);
