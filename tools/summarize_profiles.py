@@ -81,7 +81,7 @@ def main(tag):
     lines = [f"# ncu launch list, round {tag}",
              "",
              "`ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv "
-             "python bench.py --steps 1 --warmup 1 --no-c3 --e2e-steps 0 --no-cpu` (raw: "
+             "python bench.py --steps 1 --warmup 1 --no-c3 --no-c4 --no-c5 --e2e-steps 0 --no-cpu` (raw: "
              f"`launches_{tag}.csv`). Cold-cache, serialised: compare shares, not absolutes.",
              "", "| kernel | launches | mean us | share of listed time |", "|---|---:|---:|---:|"]
     for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
