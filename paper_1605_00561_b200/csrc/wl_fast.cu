@@ -60,12 +60,29 @@ void geo(int* R, int* NW, int* CPT) {
     *CPT = C::CPT;
 }
 
-void geometry(const WlLevel& L, int* R, int* NW, int* CPT) {
+// Tile geometry of the instantiation that serves (wavelet, scheme, direction)
+// -- must match the SchemeConfig the kernel was compiled with.
+template <int W, int D>
+void geo_wd(int scheme, int* R, int* NW, int* CPT) {
     using namespace wlfast;
+    switch (scheme) {
+        case 0: return geo<SchemeConfig<W, D, 0>>(R, NW, CPT);
+        case 1: return geo<SchemeConfig<W, D, 1>>(R, NW, CPT);
+        case 2: return geo<SchemeConfig<W, D, 2>>(R, NW, CPT);
+        case 3: return geo<SchemeConfig<W, D, 3>>(R, NW, CPT);
+        case 4: return geo<SchemeConfig<W, D, 4>>(R, NW, CPT);
+        case 5: return geo<SchemeConfig<W, D, 5>>(R, NW, CPT);
+        case 6: return geo<SchemeConfig<W, D, 6>>(R, NW, CPT);
+        case 7: return geo<SchemeConfig<W, D, 7>>(R, NW, CPT);
+        default: return geo<SchemeConfig<W, D, 8>>(R, NW, CPT);
+    }
+}
+
+void geometry(const WlLevel& L, int* R, int* NW, int* CPT) {
     if (L.wavelet == 0)
-        L.direction == 0 ? geo<Config<0, 0>>(R, NW, CPT) : geo<Config<0, 1>>(R, NW, CPT);
+        L.direction == 0 ? geo_wd<0, 0>(L.scheme, R, NW, CPT) : geo_wd<0, 1>(L.scheme, R, NW, CPT);
     else
-        L.direction == 0 ? geo<Config<1, 0>>(R, NW, CPT) : geo<Config<1, 1>>(R, NW, CPT);
+        L.direction == 0 ? geo_wd<1, 0>(L.scheme, R, NW, CPT) : geo_wd<1, 1>(L.scheme, R, NW, CPT);
 }
 
 bool aligned(const void* p, int bytes) { return (reinterpret_cast<uintptr_t>(p) % bytes) == 0; }

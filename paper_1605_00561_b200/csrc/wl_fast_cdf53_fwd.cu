@@ -3,11 +3,13 @@
 
 cudaError_t wl_fast_cdf53_fwd(int scheme, const WlLevel& L, const wlfast::Plan& p,
                               cudaStream_t s) {
-    using C = wlfast::Config<0, 0>;
     switch (scheme) {
 #define WL_CASE(wi, si, d, P) \
     case si:                  \
-        return wlfast::launch<P, d, C::R, C::NW, C::CPT, C::NS>(L, p, s);
+        return wlfast::launch<P, d, wlfast::SchemeConfig<wi, d, si>::R,                    \
+                              wlfast::SchemeConfig<wi, d, si>::NW,                   \
+                              wlfast::SchemeConfig<wi, d, si>::CPT,                  \
+                              wlfast::SchemeConfig<wi, d, si>::NS>(L, p, s);
         WL_FAST_FOREACH_0_0(WL_CASE)
 #undef WL_CASE
         default:

@@ -722,6 +722,24 @@ struct Config<1, 1> {  // cdf97 inverse
     static constexpr int R = WL_R97I, NW = WL_NW97I, CPT = WL_CPT_INV, NS = WL_NS97I;
 };
 
+// Per-scheme override of the geometry (scheme = SchemeKind index). The cdf97
+// Polyphase inverse (one 126-MAC neighbour epoch: FP32-issue heavy) runs 26-30%
+// faster with the forwards' CPT = 4 layout; Polyphase* and cdf53 do not gain
+// (profiles/tuning_r01_poly_inv.txt).
+#ifndef WL_POLY_INV_CPT4
+#define WL_POLY_INV_CPT4 1
+#endif
+template <int WAVELET, int DIR, int SCHEME>
+struct SchemeConfig : Config<WAVELET, DIR> {};
+#if WL_POLY_INV_CPT4
+template <int SCHEME>
+struct PolyInv {
+    static constexpr int R = 4, NW = 8, CPT = 4, NS = 2;
+};
+template <>
+struct SchemeConfig<1, 1, 7> : PolyInv<7> {};  // cdf97 polyphase inverse
+#endif
+
 struct Plan {
     FastArgs args;
     int tiles_y;
