@@ -67,6 +67,9 @@ __global__ void __launch_bounds__(NT) conv_fast_kernel(const __grid_constant__ C
     const int r0 = a.ylo + blockIdx.y * TQY, c0 = blockIdx.x * TQX;
     const int b = blockIdx.z;
     const float* img = a.img + b * a.in_bstride;
+    // previous grid complete (PDL launch); no-op otherwise. No early trigger:
+    // this grid is not persistent, dependents must not take its SM slots.
+    wlfast::pdl_wait();
     const int py0 = 2 * r0 + C::kRow0, px0 = 2 * c0 - MARGIN;
     const bool interior = a.has_map && py0 >= 0 && px0 >= 0 && py0 + G::kRows <= h &&
                           px0 + SW <= w;
@@ -173,9 +176,9 @@ cudaError_t launch_conv(const WlLevel& L, cudaStream_t stream) {
         attr[dev & 63] = true;
     }
     const dim3 grid((L.qw + TQX - 1) / TQX, (a.yhi - a.ylo + TQY - 1) / TQY, nb);
-    conv_fast_kernel<C><<<grid, NT, smem, stream>>>(m, a);
+    cudaError_t le = wlfast::launch_pdl(conv_fast_kernel<C>, grid, dim3(NT), smem, stream, m, a);
     wl_count_launch();
-    return cudaGetLastError();
+    return le != cudaSuccess ? le : cudaGetLastError();
 }
 
 }  // namespace

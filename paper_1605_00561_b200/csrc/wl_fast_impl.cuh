@@ -164,6 +164,34 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* b, unsigned parity) {
 #define WL_STORE_PAIRS 0
 #endif
 
+// Programmatic dependent launch: wait until the preceding grid in the stream
+// has completed and its writes are visible (no-op for normal launches), and
+// let the next PDL-launched grid get scheduled while this one drains.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+#ifndef WL_PDL
+#define WL_PDL 0  // measured 3.7% slower on the bench step (profiles/tuning_r01_pdl.txt)
+#endif
+
+// Launch with the programmatic-stream-serialization attribute (PDL).
+template <class K, class... Args>
+cudaError_t launch_pdl(K kern, dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                       Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = WL_PDL;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 __device__ __forceinline__ void named_sync(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
@@ -259,6 +287,10 @@ __global__ void __launch_bounds__((NW + 1) * 32, (Geometry<R, NW, CPT, NS>::kMin
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
+    // everything above touched shared memory only: overlap it with the
+    // previous kernel's tail, then order all global traffic after it
+    pdl_wait();
+    pdl_trigger();
 
     if (warp == NW) {
         // ---------------- producer warp: TMA tile stream ----------------
@@ -862,9 +894,10 @@ cudaError_t launch(const WlLevel& L, const Plan& plan, cudaStream_t stream) {
         mb = (per_sm > 0 ? per_sm : 1) * sms;
     }
     const int grid = a.ntiles < mb ? a.ntiles : mb;
-    kern<<<grid, (NW + 1) * 32, G::kSmemBytes, stream>>>(maps[0], maps[1], maps[2], maps[3], a);
+    cudaError_t le = launch_pdl(kern, dim3(grid), dim3((NW + 1) * 32), G::kSmemBytes, stream,
+                                maps[0], maps[1], maps[2], maps[3], a);
     wl_count_launch();
-    return cudaGetLastError();
+    return le != cudaSuccess ? le : cudaGetLastError();
 }
 
 }  // namespace wlfast
