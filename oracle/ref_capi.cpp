@@ -14,8 +14,10 @@
 //   boundary 0 periodic, 1 symmetric            (transform.hpp:44)
 // Status: 0 ok, 1 std::invalid_argument, 2 any other exception.
 
+#include "wavelift/pgm.hpp"
 #include "wavelift/polyphase.hpp"
 #include "wavelift/schemes.hpp"
+#include "wavelift/subband_io.hpp"
 #include "wavelift/transform.hpp"
 #include "wavelift/wavelets.hpp"
 
@@ -293,6 +295,113 @@ int wlref_verify_identity(int wavelet, int scheme, double* max_dev, int* match) 
             w.mode() == CoeffMode::exact ? 0.0 : 1e-12);
         *max_dev = rep.max_deviation;
         *match = rep.match ? 1 : 0;
+    });
+}
+
+
+// ---- file formats (pgm.cpp, subband_io.cpp) and the CLI's cmd_transform
+// (wavelift_main.cpp:153-177), through the unmodified reference library.
+// Pyramids cross the ABI in the B200 flat layout: per level HL, LH, HH
+// (finest first), then the coarsest LL.
+
+int wlref_write_pgm(const char* path, int w, int h, int maxval, const unsigned short* px) {
+    return guarded([&] {
+        PgmImage p;
+        p.width = w;
+        p.height = h;
+        p.maxval = maxval;
+        p.pixels.assign(px, px + static_cast<std::size_t>(w) * h);
+        write_pgm(path, p);
+    });
+}
+
+// Two-call pattern: px may be null to query the size.
+int wlref_read_pgm(const char* path, int* w, int* h, int* maxval, unsigned short* px) {
+    return guarded([&] {
+        const PgmImage p = read_pgm(path);
+        *w = p.width;
+        *h = p.height;
+        *maxval = p.maxval;
+        if (px) std::memcpy(px, p.pixels.data(), p.pixels.size() * sizeof(unsigned short));
+    });
+}
+
+static Pyramid pyramid_from_flat(const double* flat, int w, int h, int levels) {
+    Pyramid p;
+    std::size_t off = 0;
+    for (int l = 0; l < levels; ++l) {
+        PyramidLevel lv;
+        lv.w = w >> (l + 1);
+        lv.h = h >> (l + 1);
+        const std::size_t n = static_cast<std::size_t>(lv.w) * lv.h;
+        lv.hl.assign(flat + off, flat + off + n);
+        lv.lh.assign(flat + off + n, flat + off + 2 * n);
+        lv.hh.assign(flat + off + 2 * n, flat + off + 3 * n);
+        off += 3 * n;
+        p.details.push_back(std::move(lv));
+    }
+    p.ll_w = w >> levels;
+    p.ll_h = h >> levels;
+    p.ll.assign(flat + off, flat + off + static_cast<std::size_t>(p.ll_w) * p.ll_h);
+    return p;
+}
+
+int wlref_write_subbands(const char* path, const char* wavelet, const char* scheme, int levels,
+                         int boundary, int scaling, int w, int h, const double* flat) {
+    return guarded([&] {
+        SubbandHeader hd;
+        hd.wavelet = wavelet;
+        hd.scheme = scheme;
+        hd.levels = levels;
+        hd.boundary = boundary_mode(boundary);
+        hd.scaling = scaling != 0;
+        hd.image_w = w;
+        hd.image_h = h;
+        write_subbands(path, hd, pyramid_from_flat(flat, w, h, levels));
+    });
+}
+
+// header out-params; flat (w*h doubles) may be null to query the header.
+int wlref_read_subbands(const char* path, char* wavelet64, char* scheme64, int* levels,
+                        int* boundary, int* scaling, int* w, int* h, double* flat) {
+    return guarded([&] {
+        const auto [hd, p] = read_subbands(path);
+        std::snprintf(wavelet64, 64, "%s", hd.wavelet.c_str());
+        std::snprintf(scheme64, 64, "%s", hd.scheme.c_str());
+        *levels = hd.levels;
+        *boundary = hd.boundary == BoundaryMode::periodic ? 0 : 1;
+        *scaling = hd.scaling ? 1 : 0;
+        *w = hd.image_w;
+        *h = hd.image_h;
+        if (!flat) return;
+        std::size_t off = 0;
+        for (const PyramidLevel& lv : p.details)
+            for (const auto* pl : {&lv.hl, &lv.lh, &lv.hh}) {
+                std::memcpy(flat + off, pl->data(), pl->size() * sizeof(double));
+                off += pl->size();
+            }
+        std::memcpy(flat + off, p.ll.data(), p.ll.size() * sizeof(double));
+    });
+}
+
+// cmd_transform without --pad: PGM -> multi_level_forward -> subband file.
+int wlref_transform_file(const char* in, const char* out, int wavelet, int scheme, int levels,
+                         int boundary, int scaling) {
+    return guarded([&] {
+        const Image img = wavelift::to_image(read_pgm(in));
+        const WaveletSpec wv = get_wavelet(wavelet_name(wavelet));
+        const SchemeKind kind = scheme_kind(scheme);
+        const Pyramid p = multi_level_forward(img, build_scheme(kind, wv), levels,
+                                              boundary_mode(boundary), scaling != 0);
+        SubbandHeader hd;
+        hd.wavelet = wv.name;
+        hd.scheme = scheme_name(kind);
+        hd.levels = levels;
+        hd.boundary = boundary_mode(boundary);
+        hd.scaling = scaling != 0;
+        hd.image_w = img.width;
+        hd.image_h = img.height;
+        write_subbands(out, hd, p);
     });
 }
 

@@ -81,6 +81,27 @@ def build_lib(verbose=False) -> str:
     return LIB
 
 
+CLI_SRC = os.path.join(PKG, "cli", "wavelift_b200.cpp")
+CLI_BIN = os.path.join(PKG, "bin", "wavelift_b200")
+
+
+def build_cli() -> str:
+    """The wavelift_b200 CLI (host C++ over the C-ABI library)."""
+    deps = [CLI_SRC, LIB, os.path.join(ROOT, "include", "wavelift_b200.hpp"),
+            os.path.join(ROOT, "include", "wavelift_b200_io.hpp")]
+    if not _newer(CLI_BIN, deps):
+        return CLI_BIN
+    os.makedirs(os.path.dirname(CLI_BIN), exist_ok=True)
+    cmd = ["g++", "-std=c++17", "-O2", "-Wall", "-Wextra", "-o", CLI_BIN, CLI_SRC,
+           "-I" + os.path.join(ROOT, "include"), "-I/usr/local/cuda/include", "-L" + PKG,
+           "-lwavelift_b200", "-L/usr/local/cuda/lib64", "-lcudart",
+           "-Wl,-rpath,$ORIGIN/..:/usr/local/cuda/lib64"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"CLI build failed:\n{r.stdout}\n{r.stderr}")
+    return CLI_BIN
+
+
 def build_oracle():
     r = subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle")], capture_output=True,
                        text=True)
@@ -90,7 +111,10 @@ def build_oracle():
 
 def build(verbose=False):
     build_oracle()
-    return build_lib(verbose)
+    lib = build_lib(verbose)
+    if not VARIANT:
+        build_cli()
+    return lib
 
 
 if __name__ == "__main__":
