@@ -9,7 +9,9 @@ cudaError_t wl_fast_cdf53_fwd(int scheme, const WlLevel& L, const wlfast::Plan& 
         return wlfast::launch<P, d, wlfast::SchemeConfig<wi, d, si>::R,                    \
                               wlfast::SchemeConfig<wi, d, si>::NW,                   \
                               wlfast::SchemeConfig<wi, d, si>::CPT,                  \
-                              wlfast::SchemeConfig<wi, d, si>::NS>(L, p, s);
+                              wlfast::SchemeConfig<wi, d, si>::NS,                   \
+                              wlfast::SchemeConfig<wi, d, si>::XF,                   \
+                              wlfast::SchemeConfig<wi, d, si>::MAXB>(L, p, s);
         WL_FAST_FOREACH_0_0(WL_CASE)
 #undef WL_CASE
         default:

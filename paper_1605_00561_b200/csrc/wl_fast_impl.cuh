@@ -44,6 +44,12 @@ namespace wlfast {
 // Producer wait on a released stage: 0 = test_wait + __nanosleep back-off
 // (cap WL_PROD_BACKOFF_NS), 1 = try_wait with a suspend hint, 2 = plain
 // try_wait loop (hardware-timed suspend).
+// Tuning knobs: pad the exchange buffer to at least this many component rows
+// (shared-memory footprint / residency experiments) and cap CTAs per SM
+// (0 = as many as fit).
+#ifndef WL_XCH_MIN
+#define WL_XCH_MIN 0
+#endif
 #ifndef WL_PROD_SLEEP
 #define WL_PROD_SLEEP 0
 #endif
@@ -54,12 +60,6 @@ namespace wlfast {
 #define WL_PROD_BACKOFF_NS 256
 #endif
 
-// Edge exchange between compute warps: 0 = one bar.sync per epoch (default),
-// 1 = split-phase mbarrier (arrive after publishing, wait before the edge
-// rows). Both execute one barrier per epoch; kept switchable for A/B runs.
-#ifndef WL_XCH_MBAR
-#define WL_XCH_MBAR 0
-#endif
 
 // CPT = component cells per lane per row (2 or 4); the compute region is
 // 32 * CPT cells wide. CPT = 4 stores one aligned float4 per lane and plane
@@ -214,14 +214,16 @@ struct FastArgs {
     int ylo, yhi;        // stored cell rows [ylo, yhi); out[] addresses row ylo
 };
 
-template <int R, int NW, int CPT, int NS = 2>
+template <int R, int NW, int CPT, int NS = 2, int NXC = 4>
 struct Geometry {
     static constexpr int kStages = NS;                       // TMA ring depth
     static constexpr int TWC = 32 * CPT;                     // compute-region width in cells
     static constexpr int kRows = NW * R + 2;                 // cell rows per stage incl. ghosts
     static constexpr int kStageFloats = 4 * TWC * kRows;     // == 2*TWC px * 2*kRows px
     static constexpr int kStageBytes = kStageFloats * 4;
-    static constexpr int kXchFloats = 2 * NW * 2 * 32 * CPT * 4;
+    // edge exchange: 2 slots x NW warps x NXC published component rows of
+    // 32 * CPT cells (NXC = the most components any epoch reads across warps)
+    static constexpr int kXchFloats = 2 * NW * (NXC > WL_XCH_MIN ? NXC : WL_XCH_MIN) * 32 * CPT;
     static constexpr size_t kSmemBytes =
         NS * (size_t)kStageBytes + (size_t)kXchFloats * 4 + 16 * NS;
     // CTAs per SM the shared memory allows (228 KB per SM, 1 KB reserved per CTA)
@@ -262,13 +264,49 @@ __host__ __device__ constexpr bool uses_dc(unsigned long long m, int c, int dc) 
 __host__ __device__ constexpr bool uses_dr(unsigned long long m, int c, int dr) {
     return uses(m, c, dr, -1) || uses(m, c, dr, 0) || uses(m, c, dr, 1);
 }
+// number of components read from the row above (dr = -1) / below (dr = +1)
+__host__ __device__ constexpr int n_dr(unsigned long long m, int dr) {
+    int n = 0;
+    for (int c = 0; c < 4; ++c) n += uses_dr(m, c, dr) ? 1 : 0;
+    return n;
+}
+// Exchange mode: minimal (publish only the component rows the neighbour
+// warps read this epoch: a lifting epoch reads across warps from one side
+// only, 2 components; Polyphase up to 6) or full (both edge rows, all 4
+// components). Chosen per configuration by measurement (Config::kFullXch).
+__host__ __device__ constexpr bool xch_up(unsigned long long m, int c, bool full) {
+    return full || uses_dr(m, c, -1);
+}
+__host__ __device__ constexpr bool xch_dn(unsigned long long m, int c, bool full) {
+    return full || uses_dr(m, c, 1);
+}
+__host__ __device__ constexpr int xch_rank(unsigned long long m, int c, int dr, bool full) {
+    int n = 0;
+    for (int k = 0; k < c; ++k) n += (dr < 0 ? xch_up(m, k, full) : xch_dn(m, k, full)) ? 1 : 0;
+    return n;
+}
+__host__ __device__ constexpr int xch_count(unsigned long long m, int dr, bool full) {
+    return xch_rank(m, 4, dr, full);
+}
+template <class P, bool FULL>
+constexpr int xch_comps() {
+    if (FULL) return P::kEpochs > 1 ? 8 : 0;
+    int mx = 0;
+    for (int e = 1; e < P::kEpochs; ++e) {
+        const int n = n_dr(P::kUse[e], -1) + n_dr(P::kUse[e], 1);
+        mx = n > mx ? n : mx;
+    }
+    return mx;
+}
 
-template <class P, int DIR, int R, int NW, int CPT, int NS>
-__global__ void __launch_bounds__((NW + 1) * 32, (Geometry<R, NW, CPT, NS>::kMinBlocks))
+template <class P, int DIR, int R, int NW, int CPT, int NS, bool XF>
+__global__ void __launch_bounds__((NW + 1) * 32,
+                                  (Geometry<R, NW, CPT, NS, xch_comps<P, XF>()>::kMinBlocks))
     fast_kernel(const __grid_constant__ CUtensorMap m0, const __grid_constant__ CUtensorMap m1,
                 const __grid_constant__ CUtensorMap m2, const __grid_constant__ CUtensorMap m3,
                 const FastArgs a) {
-    using G = Geometry<R, NW, CPT, NS>;
+    constexpr int NXC = xch_comps<P, XF>();
+    using G = Geometry<R, NW, CPT, NS, NXC>;
     constexpr int H = P::kHalo;
     constexpr int TWC = G::TWC;
     constexpr int HX = halo_x<CPT, H>();
@@ -336,7 +374,6 @@ __global__ void __launch_bounds__((NW + 1) * 32, (Geometry<R, NW, CPT, NS>::kMin
     float v[R][CPT][4];
     float gu[CPT][4], gd[CPT][4];
     int xslot = 0;
-    unsigned xphase = 0;  // parity of the next phase to wait for, per slot (bit s)
 
     for (int i = 0, t = blockIdx.x; t < a.ntiles; t += gridDim.x, ++i) {
         const int s = i % NS;
@@ -477,26 +514,44 @@ __global__ void __launch_bounds__((NW + 1) * 32, (Geometry<R, NW, CPT, NS>::kMin
             // barrier (one mbarrier phase) per epoch per tile.
             // Layout [slot][warp][top|bottom][column c][lane] float4: every
             // warp-wide access is a contiguous 512 B run (4 wavefronts).
-            constexpr int kRowF = CPT * 32 * 4;  // floats per published row
-            float* xw = xch + (xslot * NW + warp) * 2 * kRowF;
-            if constexpr (E > 0) {
-#pragma unroll
-                for (int c = 0; c < CPT; ++c) {
-                    reinterpret_cast<float4*>(xw + c * 128)[lane] =
-                        make_float4(v[0][c][0], v[0][c][1], v[0][c][2], v[0][c][3]);
-                    reinterpret_cast<float4*>(xw + kRowF + c * 128)[lane] = make_float4(
-                        v[R - 1][c][0], v[R - 1][c][1], v[R - 1][c][2], v[R - 1][c][3]);
+            // Published component rows of this epoch: the warp's bottom row for
+            // the components the warp below reads from its row above (UP), then
+            // its top row for those the warp above reads from below (DN). Each
+            // row is [lane] x CPT floats: one contiguous warp-wide access.
+            constexpr int NUP = xch_count(U, -1, XF), NDN = xch_count(U, 1, XF);
+            constexpr int kCompF = 32 * CPT;
+            constexpr int kSlotF = NXC * kCompF;
+            float* xw = xch + (xslot * NW + warp) * kSlotF;
+            auto put = [&](float* dst, const float (&row)[CPT][4], int C) {
+                if constexpr (CPT == 4)
+                    reinterpret_cast<float4*>(dst)[lane] =
+                        make_float4(row[0][C], row[1][C], row[2][C], row[3][C]);
+                else
+                    reinterpret_cast<float2*>(dst)[lane] = make_float2(row[0][C], row[1][C]);
+            };
+            auto get = [&](const float* src, float (&row)[CPT][4], int C) {
+                if constexpr (CPT == 4) {
+                    const float4 q = reinterpret_cast<const float4*>(src)[lane];
+                    row[0][C] = q.x; row[1][C] = q.y; row[2][C] = q.z; row[3][C] = q.w;
+                } else {
+                    const float2 q = reinterpret_cast<const float2*>(src)[lane];
+                    row[0][C] = q.x; row[1][C] = q.y;
                 }
-#if WL_XCH_MBAR
-                mbar_arrive(&xbar[xslot]);  // release: this lane's edge stores
-#else
+            };
+            if constexpr (E > 0) {
+                sfor<4>([&](auto c_) {
+                    constexpr int C = decltype(c_)::value;
+                    if constexpr (xch_up(U, C, XF))
+                        put(xw + xch_rank(U, C, -1, XF) * kCompF, v[R - 1], C);
+                    if constexpr (xch_dn(U, C, XF))
+                        put(xw + (NUP + xch_rank(U, C, 1, XF)) * kCompF, v[0], C);
+                });
 #ifdef WL_BREAK_BARRIER
                 // negative control (acceptance.cpp:283-296 / parsim break_barrier):
                 // drop the barrier of epoch WL_BREAK_BARRIER; racecheck must flag it
                 if constexpr (E != WL_BREAK_BARRIER)
 #endif
                 named_sync(1, NW * 32);  // the epoch's block barrier
-#endif
             }
             // Horizontal neighbours of the lane's edge columns (warp shuffle).
             float sl[R + 2][4], sr[R + 2][4];
@@ -524,26 +579,15 @@ __global__ void __launch_bounds__((NW + 1) * 32, (Geometry<R, NW, CPT, NS>::kMin
             // interior rows 1..R-2 read only this warp's rows
             sfor<R - 2>([&](auto r_) { row(std::integral_constant<int, decltype(r_)::value + 1>{}); });
             if constexpr (E > 0) {
-#if WL_XCH_MBAR
-                mbar_wait(&xbar[xslot], (xphase >> xslot) & 1);
-                xphase ^= 1u << xslot;
-#endif
-                if (warp > 0) {  // bottom row of the warp above
-                    const float* nb = xw - 2 * kRowF + kRowF;
-#pragma unroll
-                    for (int c = 0; c < CPT; ++c) {
-                        const float4 q = reinterpret_cast<const float4*>(nb + c * 128)[lane];
-                        gu[c][0] = q.x; gu[c][1] = q.y; gu[c][2] = q.z; gu[c][3] = q.w;
-                    }
-                }
-                if (warp < NW - 1) {  // top row of the warp below
-                    const float* nb = xw + 2 * kRowF;
-#pragma unroll
-                    for (int c = 0; c < CPT; ++c) {
-                        const float4 q = reinterpret_cast<const float4*>(nb + c * 128)[lane];
-                        gd[c][0] = q.x; gd[c][1] = q.y; gd[c][2] = q.z; gd[c][3] = q.w;
-                    }
-                }
+                sfor<4>([&](auto c_) {
+                    constexpr int C = decltype(c_)::value;
+                    if constexpr (xch_up(U, C, XF))  // bottom row of the warp above
+                        if (warp > 0) get(xw - kSlotF + xch_rank(U, C, -1, XF) * kCompF, gu, C);
+                    if constexpr (xch_dn(U, C, XF))  // top row of the warp below
+                        if (warp < NW - 1)
+                            get(xw + kSlotF + (NUP + xch_rank(U, C, 1, XF)) * kCompF, gd, C);
+                });
+                (void)NDN;
                 xslot ^= 1;
             }
             sfor<4>([&](auto c_) {
@@ -701,6 +745,25 @@ struct Config;
 #ifndef WL_CPT_INV
 #define WL_CPT_INV 2
 #endif
+// exchange mode (1 = full) and CTAs-per-SM cap (0 = none) per configuration
+#ifndef WL_XF53F
+#define WL_XF53F 1
+#endif
+#ifndef WL_XF53I
+#define WL_XF53I 0
+#endif
+#ifndef WL_XF97F
+#define WL_XF97F 0
+#endif
+#ifndef WL_XF97I
+#define WL_XF97I 0
+#endif
+#ifndef WL_MAXB53I
+#define WL_MAXB53I 0
+#endif
+#ifndef WL_MAXB97I
+#define WL_MAXB97I 2
+#endif
 #ifndef WL_NS53F
 #define WL_NS53F 3
 #endif
@@ -740,18 +803,26 @@ struct Config;
 template <>
 struct Config<0, 0> {  // cdf53 forward, halo 1
     static constexpr int R = WL_R53F, NW = WL_NW53F, CPT = WL_CPT_FWD, NS = WL_NS53F;
+    static constexpr bool XF = WL_XF53F;
+    static constexpr int MAXB = 0;
 };
 template <>
 struct Config<0, 1> {  // cdf53 inverse
     static constexpr int R = WL_R53I, NW = WL_NW53I, CPT = WL_CPT_INV, NS = WL_NS53I;
+    static constexpr bool XF = WL_XF53I;
+    static constexpr int MAXB = WL_MAXB53I;
 };
 template <>
 struct Config<1, 0> {  // cdf97 forward, halo 2
     static constexpr int R = WL_R97F, NW = WL_NW97F, CPT = WL_CPT_FWD, NS = WL_NS97F;
+    static constexpr bool XF = WL_XF97F;
+    static constexpr int MAXB = 0;
 };
 template <>
 struct Config<1, 1> {  // cdf97 inverse
     static constexpr int R = WL_R97I, NW = WL_NW97I, CPT = WL_CPT_INV, NS = WL_NS97I;
+    static constexpr bool XF = WL_XF97I;
+    static constexpr int MAXB = WL_MAXB97I;
 };
 
 // Per-scheme override of the geometry (scheme = SchemeKind index). The cdf97
@@ -767,10 +838,30 @@ struct SchemeConfig : Config<WAVELET, DIR> {};
 template <int SCHEME>
 struct PolyInv {
     static constexpr int R = 4, NW = 8, CPT = 4, NS = 2;
+    static constexpr bool XF = false;
+    static constexpr int MAXB = 0;
 };
 template <>
 struct SchemeConfig<1, 1, 7> : PolyInv<7> {};  // cdf97 polyphase inverse
 #endif
+// cdf97 Polyphase forward: 6 exchanged component rows (its single neighbour
+// epoch reads 4 components above, 2 below) -- keep a 2-stage ring so the
+// CTA fits in shared memory when the other forwards use 3 stages.
+template <>
+struct SchemeConfig<1, 0, 7> : Config<1, 0> {
+    static constexpr int NS = 2;
+};
+
+// cdf97 Monolithic / Monolithic* inverses: full exchange measured faster
+// (profiles/tuning_r01_exchange.txt).
+template <>
+struct SchemeConfig<1, 1, 5> : Config<1, 1> {
+    static constexpr bool XF = true;
+};
+template <>
+struct SchemeConfig<1, 1, 6> : Config<1, 1> {
+    static constexpr bool XF = true;
+};
 
 struct Plan {
     FastArgs args;
@@ -847,9 +938,9 @@ inline Plan plan_tiles(const WlLevel& L, int H, int R, int NW, int CPT) {
     return p;
 }
 
-template <class P, int DIR, int R, int NW, int CPT, int NS>
+template <class P, int DIR, int R, int NW, int CPT, int NS, bool XF, int MAXB>
 cudaError_t launch(const WlLevel& L, const Plan& plan, cudaStream_t stream) {
-    using G = Geometry<R, NW, CPT, NS>;
+    using G = Geometry<R, NW, CPT, NS, xch_comps<P, XF>()>;
     constexpr int TWC = G::TWC;
     CUtensorMap maps[4];
     FastArgs a = plan.args;
@@ -878,7 +969,7 @@ cudaError_t launch(const WlLevel& L, const Plan& plan, cudaStream_t stream) {
     a.out_pitch = L.out_pitch;
     a.scaling = L.scaling && wl_host_program(L.prog).has_scale;
     a.scale = wl_host_program(L.prog).scale;
-    auto kern = fast_kernel<P, DIR, R, NW, CPT, NS>;
+    auto kern = fast_kernel<P, DIR, R, NW, CPT, NS, XF>;
     static int max_blocks[64] = {};
     int dev = 0;
     cudaGetDevice(&dev);
@@ -891,6 +982,8 @@ cudaError_t launch(const WlLevel& L, const Plan& plan, cudaStream_t stream) {
                                                       G::kSmemBytes);
         int sms = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const int cap = MAXB;
+        if (cap > 0 && per_sm > cap) per_sm = cap;
         mb = (per_sm > 0 ? per_sm : 1) * sms;
     }
     const int grid = a.ntiles < mb ? a.ntiles : mb;
