@@ -783,7 +783,7 @@ struct Config;
 #define WL_NW53F 8
 #endif
 #ifndef WL_R97F
-#define WL_R97F 4
+#define WL_R97F 5
 #endif
 #ifndef WL_NW97F
 #define WL_NW97F 8
@@ -845,11 +845,12 @@ template <>
 struct SchemeConfig<1, 1, 7> : PolyInv<7> {};  // cdf97 polyphase inverse
 #endif
 // cdf97 Polyphase forward: 6 exchanged component rows (its single neighbour
-// epoch reads 4 components above, 2 below) -- keep a 2-stage ring so the
-// CTA fits in shared memory when the other forwards use 3 stages.
+// epoch reads 4 components above, 2 below): 32-row tiles and a 2-stage ring
+// (profiles/tuning_r01_tiles97.txt).
 template <>
 struct SchemeConfig<1, 0, 7> : Config<1, 0> {
     static constexpr int NS = 2;
+    static constexpr int R = 4;  // 40-row tiles measured slower for Polyphase
 };
 
 // cdf97 Monolithic / Monolithic* inverses: full exchange measured faster
