@@ -86,3 +86,30 @@ def test_selection_surface():
     with pytest.raises(ValueError):
         wl.get_wavelet("haar")
     assert abs(wl.get_wavelet("cdf97").zeta - 1.149604398860241) < 1e-15
+
+
+def test_new_entry_points_validate_without_gpu():
+    """Batch / strip / host / strips-runtime entry points reject bad arguments
+    with WL_EINVAL before touching the device (reference error classes)."""
+    lib = wl.lib()
+    fp = ctypes.c_void_p(1)  # never dereferenced
+    st = lib.wl_dwt2_forward_batch(fp, 8, 8, 8, 64, -1, 0, 0, 0, 0, fp, fp, fp, fp, 4, 16, None)
+    assert st == wl.WL_EINVAL and b"batch" in lib.wl_last_error()
+    st = lib.wl_dwt2_forward_batch(fp, 8, 8, 8, 32, 2, 0, 0, 0, 0, fp, fp, fp, fp, 4, 16, None)
+    assert st == wl.WL_EINVAL and b"stride" in lib.wl_last_error()     # img stride < pitch*h
+    assert lib.wl_dwt2_forward_batch(fp, 8, 8, 8, 64, 0, 0, 0, 0, 0, fp, fp, fp, fp, 4, 16,
+                                     None) == wl.WL_OK                   # empty batch: no-op
+    st = lib.wl_dwt2_pyramid_forward_batch(fp, 24, 12, 288, 2, 3, 0, 0, 0, 0, fp, 288, fp, None)
+    assert st == wl.WL_EINVAL and b"2^levels" in lib.wl_last_error()
+    st = lib.wl_dwt2_forward_strip(fp, 64, 32, 2, 64, 1, 6, 0, fp, fp, fp, fp, 32, None)
+    assert st == wl.WL_EINVAL and b"halo" in lib.wl_last_error()       # cdf97 needs 6 rows
+    st = lib.wl_dwt2_forward_strip(fp, 64, 31, 6, 64, 1, 6, 0, fp, fp, fp, fp, 32, None)
+    assert st == wl.WL_EINVAL                                          # odd rows
+    st = lib.wl_dwt2_inverse_strip(fp, fp, fp, fp, 32, 16, 1, 32, 1, 6, 0, fp, 64, None)
+    assert st == wl.WL_EINVAL                                          # cdf97 inverse needs 3
+    st = lib.wl_dwt2_forward_host(fp, 7, 8, 7, 0, 0, 0, 0, fp, fp, fp, fp, 4)
+    assert st == wl.WL_EINVAL and b"even" in lib.wl_last_error()
+    st = lib.wl_dwt2_inverse_host(None, fp, fp, fp, 4, 4, 4, 0, 0, 0, 0, fp, 8)
+    assert st == wl.WL_EINVAL and b"null" in lib.wl_last_error()
+    assert lib.wl_pyramid_batch_scratch_elems(64, 64, 2, 3) == 3 * (32 * 32 + 16 * 16)
+    assert lib.wl_pyramid_batch_scratch_elems(64, 64, 1, 3) == 3 * 32 * 32
