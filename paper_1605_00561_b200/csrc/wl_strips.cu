@@ -158,7 +158,8 @@ struct WlStrips {
     float* lvl(char* base, int l) const { return reinterpret_cast<float*>(base + lvl_off[l]); }
     unsigned* flags(char* base) const { return reinterpret_cast<unsigned*>(base + flag_off); }
     // flag indices: 2l = from_up[l], 2l+1 = from_down[l]; 2L = done_from_up,
-    // 2L+1 = done_from_down; 2L+2 = exchange CTA counter.
+    // 2L+1 = done_from_down; 2L+2 = exchange CTA counter; 2L+3, 2L+4 =
+    // scratch flags of the warm-up launches (kMaxLevels = 16 -> index <= 36).
 };
 
 extern "C" {
@@ -223,6 +224,51 @@ int wl_strips_create(int w, int h, int rank, int nranks, int levels, int wavelet
         return sfail(WL_ERUNTIME, std::string("wl_strips_create: ") + cudaGetErrorString(e));
     }
     if (nranks == 1) s->up = s->down = s->window;
+    // Warm up every kernel the protocol launches, synchronously, BEFORE any
+    // rank can spin on a neighbour: lazy module loading and the first
+    // launch's cudaFuncSetAttribute synchronise the device, which would
+    // deadlock a stream whose exchange kernel is waiting for a neighbour
+    // whose work the host has not enqueued yet.
+    {
+        const int ww = 256, rr = 16;
+        float* tmp = nullptr;
+        const size_t img = static_cast<size_t>(rr + 2 * halo) * ww;
+        const size_t np = static_cast<size_t>(ww / 2) * (rr / 2);
+        e = cudaMalloc(&tmp, (img + 4 * np) * sizeof(float));
+        if (e == cudaSuccess) e = cudaMemset(tmp, 0, (img + 4 * np) * sizeof(float));
+        int st = WL_OK;
+        if (e == cudaSuccess) {
+            float* pl = tmp + img;
+            st = wl_dwt2_forward_strip(tmp + static_cast<size_t>(halo) * ww, ww, rr, halo, ww,
+                                       wavelet, scheme, scaling, pl, pl + np, pl + 2 * np,
+                                       pl + 3 * np, ww / 2, nullptr);
+            unsigned* f = s->flags(s->window);
+            XchArgs a{};  // zero rows; signals and waits on scratch flags at epoch 0
+            a.top = a.bot = tmp;
+            a.up_dst = a.down_dst = tmp;
+            a.n = 0;
+            a.sig_up = f + 2 * levels + 3;
+            a.sig_down = f + 2 * levels + 4;
+            a.my_a = f + 2 * levels + 3;
+            a.my_b = f + 2 * levels + 4;
+            a.epoch = 0;
+            a.counter = f + 2 * levels + 2;
+            a.err = s->err_dev;
+            exchange_kernel<<<1, 256>>>(a);
+            signal_kernel<<<1, 1>>>(f + 2 * levels + 3, f + 2 * levels + 4, 0);
+            wait_kernel<<<1, 1>>>(f + 2 * levels + 3, f + 2 * levels + 4, 0, s->err_dev);
+            e = cudaDeviceSynchronize();
+        }
+        if (tmp) cudaFree(tmp);
+        if (e != cudaSuccess || st != WL_OK) {
+            const std::string msg = e != cudaSuccess ? std::string(cudaGetErrorString(e))
+                                                     : std::string(wl_last_error());
+            cudaFree(s->window);
+            cudaFreeHost(s->err_host);
+            delete s;
+            return sfail(st != WL_OK ? st : WL_ERUNTIME, "wl_strips_create warm-up: " + msg);
+        }
+    }
     *out = s;
     return WL_OK;
 }

@@ -264,3 +264,30 @@ def test_host_buffer_transforms_equal_device_path(wl, wavelet):
                 rec_want = wl.inverse(want.cuda(), wavelet, b, True, scheme=s).cpu()
                 rec = wl.inverse_host(got.pin_memory(), wavelet, b, True, scheme=s)
                 assert torch.equal(rec, rec_want), (s, b, h, w)
+
+
+def test_strip_pyramid_large_virtual_ranks(wl):
+    """configs[3] shape at scale: 16384^2, cdf97 Monolithic*, 5 levels, 4 strips
+    (virtual ranks) == the whole-image pyramid, bit for bit."""
+    import torch
+    h = w = 16384
+    img = rand((h, w), 33)
+    sch = wl.build_scheme("monolithic_star", "cdf97")
+    want = wl.multi_level_forward(img, sch, 5).flat
+    got = _virtual_ranks(wl, img, 5, sch, 4, calls=1)
+    assert torch.equal(got, want)
+    del want, got
+    torch.cuda.empty_cache()
+
+
+def test_batch_pyramid_large(wl):
+    """configs[4] shape: 16 images of 4096^2, 3 levels, batched == single calls."""
+    import torch
+    imgs = rand((16, 4096, 4096), 34)
+    for w in ("cdf53", "cdf97"):
+        sch = wl.build_scheme("monolithic_star", w)
+        pyrs = wl.multi_level_forward_batch(imgs, sch, 3)
+        for i in (0, 7, 15):
+            assert torch.equal(pyrs[i], wl.multi_level_forward(imgs[i], sch, 3).flat), (w, i)
+        rec = wl.multi_level_inverse_batch(pyrs, 4096, 4096, 3, w, scheme="monolithic_star")
+        assert (rec - imgs).abs().max().item() <= 3e-5
