@@ -435,6 +435,8 @@ def run_c4(args, wl, ws, rank, peak):
     sp.input.copy_(torch.rand(sp.input.shape, device="cuda", generator=g))
     out = torch.empty(sp.slice_elems(), device="cuda")
     stream = torch.cuda.current_stream()
+    torch.cuda.synchronize()
+    barrier(ws)  # every rank connected and idle before the first halo wait
     for _ in range(3):
         sp.forward(out)
     torch.cuda.synchronize()
