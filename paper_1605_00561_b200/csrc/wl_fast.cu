@@ -133,7 +133,8 @@ cudaError_t wl_launch_fast(const WlLevel& L, cudaStream_t stream) {
         e = L.direction == 0 ? wl_fast_cdf97_fwd(L.scheme, L, plan, stream)
                              : wl_fast_cdf97_inv(L.scheme, L, plan, stream);
     if (e != cudaSuccess) return e;
-    if (plan.args.wrap) return cudaSuccess;  // periodic: the grid covers the image
+    // periodic, or symmetric with mirrored border tiles: the grid covers the image
+    if (plan.args.wrap || plan.args.mirror) return cudaSuccess;
     // Symmetric: the frame around the tile grid (image borders included) goes
     // to the interpreter, which mirrors every out-of-image read per step.
     const int Y0 = plan.args.Y0, X0 = plan.args.X0;

@@ -33,6 +33,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <utility>
 
@@ -160,6 +161,9 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* b, unsigned parity) {
 #ifndef WL_WRAP_MOD_INV
 #define WL_WRAP_MOD_INV 1
 #endif
+#ifndef WL_SYM_FAST
+#define WL_SYM_FAST 1
+#endif
 #ifndef WL_STORE_PAIRS
 #define WL_STORE_PAIRS 0
 #endif
@@ -212,6 +216,8 @@ struct FastArgs {
     float scale;
     long in_bstride[4], out_bstride[4];  // per plane: elements between images of a batch
     int ylo, yhi;        // stored cell rows [ylo, yhi); out[] addresses row ylo
+    int mirror;          // symmetric plan covering the whole image (border tiles mirror)
+    int filter;          // 0 every tile, 1 interior tiles only, 2 border tiles only
 };
 
 template <int R, int NW, int CPT, int NS = 2, int NXC = 4>
@@ -274,6 +280,10 @@ __host__ __device__ constexpr int n_dr(unsigned long long m, int dr) {
 // warps read this epoch: a lifting epoch reads across warps from one side
 // only, 2 components; Polyphase up to 6) or full (both edge rows, all 4
 // components). Chosen per configuration by measurement (Config::kFullXch).
+// Exchange mode: minimal (publish only the component rows the neighbour
+// warps read this epoch: a lifting epoch reads across warps from one side
+// only, 2 components; Polyphase up to 6) or full (both edge rows, all 4
+// components). Chosen per configuration by measurement (Config::kFullXch).
 __host__ __device__ constexpr bool xch_up(unsigned long long m, int c, bool full) {
     return full || uses_dr(m, c, -1);
 }
@@ -299,7 +309,7 @@ constexpr int xch_comps() {
     return mx;
 }
 
-template <class P, int DIR, int R, int NW, int CPT, int NS, bool XF>
+template <class P, int DIR, int R, int NW, int CPT, int NS, bool XF, bool MIRROR>
 __global__ void __launch_bounds__((NW + 1) * 32,
                                   (Geometry<R, NW, CPT, NS, xch_comps<P, XF>()>::kMinBlocks))
     fast_kernel(const __grid_constant__ CUtensorMap m0, const __grid_constant__ CUtensorMap m1,
@@ -333,7 +343,15 @@ __global__ void __launch_bounds__((NW + 1) * 32,
     if (warp == NW) {
         // ---------------- producer warp: TMA tile stream ----------------
         if (lane == 0) {
-            for (int i = 0, t = blockIdx.x; t < a.ntiles; t += gridDim.x, ++i) {
+            for (int i = 0, t = blockIdx.x; t < a.ntiles; t += gridDim.x) {
+                if (a.filter) {  // interior-only / border-only launch of a symmetric plan
+                    const int fb = t / a.ntiles_img, ft = t - fb * a.ntiles_img;
+                    const int fy = ft / a.tiles_x;
+                    const int fx0 = a.X0 + (ft - fy * a.tiles_x + a.tx0) * a.TW - HX;
+                    const int fy0 = a.Y0 + (fy + a.ty0) * a.TH - H - 1;
+                    const bool bd = fx0 < 0 || fy0 < 0 || fx0 + TWC > a.qw || fy0 + G::kRows > a.qh;
+                    if (bd != (a.filter == 2)) continue;
+                }
                 const int s = i % NS;
                 const unsigned use = i / NS;  // how often stage s was filled before
                 if (i >= NS) {
@@ -365,6 +383,7 @@ __global__ void __launch_bounds__((NW + 1) * 32,
                     tma_load_3d(dst + 2 * plane, &m2, &full[s], cx, cy, b);
                     tma_load_3d(dst + 3 * plane, &m3, &full[s], cx, cy, b);
                 }
+                ++i;
             }
         }
         return;
@@ -375,19 +394,27 @@ __global__ void __launch_bounds__((NW + 1) * 32,
     float gu[CPT][4], gd[CPT][4];
     int xslot = 0;
 
-    for (int i = 0, t = blockIdx.x; t < a.ntiles; t += gridDim.x, ++i) {
+    for (int i = 0, t = blockIdx.x; t < a.ntiles; t += gridDim.x) {
         const int s = i % NS;
         const int b = t / a.ntiles_img, tt = t - b * a.ntiles_img;
         const int tyi = tt / a.tiles_x;
         const int ty = tyi + a.ty0, tx = tt - tyi * a.tiles_x + a.tx0;
         const int cx = a.X0 + tx * a.TW - HX;     // first compute cell column
         const int cy = a.Y0 + ty * a.TH - H - 1;  // ghost row above the region
-        // Periodic border tile (only when the plan covers the whole image):
-        // its cells are loaded with wrapped coordinates straight from global
-        // memory -- load-time wrap is exact for the periodic extension.
-        const bool wrap_tile =
-            a.wrap && (cx < 0 || cy < 0 || cx + TWC > a.qw || cy + G::kRows > a.qh);
-        mbar_wait(&full[s], (i / NS) & 1);
+        // Border tile: its compute region leaves the image. Periodic plans
+        // load its cells with wrapped coordinates straight from global memory
+        // (load-time wrap is exact for the periodic extension).
+        const bool border = cx < 0 || cy < 0 || cx + TWC > a.qw || cy + G::kRows > a.qh;
+        if (a.filter && border != (a.filter == 2)) continue;  // the other launch's tile
+        const unsigned phase = (i / NS) & 1;  // fill count of stage s (processed tiles)
+        ++i;
+        const bool wrap_tile = a.wrap && border;
+        // Symmetric border tile: out-of-image cells come zero-filled from the
+        // TMA box and are never read as such -- before every neighbour step
+        // the distance-1 ghosts are overwritten with their mirror images.
+        const bool mtile = MIRROR && a.mirror && border;
+        const int gy0m = cy + 1 + warp * R;  // image row of v[0]
+        mbar_wait(&full[s], phase);
         const float* st = stage + s * G::kStageFloats;
 
         // Load the warp's rows (+ one ghost row above and below) and split
@@ -553,6 +580,68 @@ __global__ void __launch_bounds__((NW + 1) * 32,
 #endif
                 named_sync(1, NW * 32);  // the epoch's block barrier
             }
+            // Symmetric border tiles (MIRROR kernel): whole-point mirroring on
+            // the component grid, per step (transform.cpp:66-71, 114-115).
+            // Every step reads at most one cell away, so before the step the
+            // distance-1 ghosts that in-image cells read are overwritten with
+            // their mirror images: row -1 := row 1, row qh := row qh-2,
+            // column -1 := column 1, column qw := column qw-2 (corners via
+            // both). The host picks the grid's row offset so that the source
+            // rows always lie in the warp's own registers (plan_tiles).
+            // vrow(T): block row T in [-1, R] (gu, v[0..R-1], gd).
+            auto vfix = [&](auto gdgu) {  // gdgu: false -> targets in v, true -> gu/gd
+                if (!mtile) return;
+                const int t_top = -gy0m - 1;  // block row holding image row -1
+                const int t_bot = a.qh - gy0m;  // block row holding image row qh
+                sfor<R + 2>([&](auto k_) {
+                    constexpr int T = decltype(k_)::value - 1;
+                    constexpr bool edge = T < 0 || T >= R;
+                    if constexpr (edge == decltype(gdgu)::value) {
+                        float (&dst)[CPT][4] = T < 0 ? gu : (T >= R ? gd : v[T < 0 ? 0 : (T >= R ? R - 1 : T)]);
+                        if constexpr (T + 2 <= R - 1) {
+                            if (T == t_top)
+                                sfor<4>([&](auto c_) {
+                                    constexpr int C = decltype(c_)::value;
+                                    if constexpr (uses_dr(U, C, -1))
+#pragma unroll
+                                        for (int c = 0; c < CPT; ++c) dst[c][C] = v[T + 2][c][C];
+                                });
+                        }
+                        if constexpr (T - 2 >= 0) {
+                            if (T == t_bot)
+                                sfor<4>([&](auto c_) {
+                                    constexpr int C = decltype(c_)::value;
+                                    if constexpr (uses_dr(U, C, 1))
+#pragma unroll
+                                        for (int c = 0; c < CPT; ++c) dst[c][C] = v[T - 2][c][C];
+                                });
+                        }
+                    }
+                });
+            };
+            // horizontal: the lane whose first cell is column 0 reads its left
+            // neighbour as its own column 1; the lane whose last cell is column
+            // qw-1 reads its right neighbour as its own column qw-2 (cx and qw
+            // are multiples of CPT).
+            auto hfix = [&](float (&sl_)[R + 2][4], float (&sr_)[R + 2][4], int r_lo, int r_hi) {
+                if (!mtile) return;
+                const int gxl = cx + CPT * lane;
+                const bool left = gxl == 0, right = gxl + CPT - 1 == a.qw - 1;
+#pragma unroll
+                for (int r = 0; r < R + 2; ++r) {
+                    if (r < r_lo || r > r_hi) continue;
+                    const float (&src)[CPT][4] =
+                        r == 0 ? gu : (r == R + 1 ? gd : v[r == 0 ? 0 : (r > R ? R - 1 : r - 1)]);
+                    sfor<4>([&](auto c_) {
+                        constexpr int C = decltype(c_)::value;
+                        if constexpr (uses_dc(U, C, -1))
+                            if (left) sl_[r][C] = src[1][C];
+                        if constexpr (uses_dc(U, C, 1))
+                            if (right) sr_[r][C] = src[CPT - 2][C];
+                    });
+                }
+            };
+            if constexpr (MIRROR) vfix(std::false_type{});
             // Horizontal neighbours of the lane's edge columns (warp shuffle).
             float sl[R + 2][4], sr[R + 2][4];
             sfor<4>([&](auto c_) {
@@ -568,6 +657,7 @@ __global__ void __launch_bounds__((NW + 1) * 32,
                         sr[r + 1][C] = __shfl_down_sync(0xffffffffu, v[r][0][C], 1);
                 }
             });
+            if constexpr (MIRROR) hfix(sl, sr, 1, R);
             float o[R][CPT][4];
             auto row = [&](auto r_) {
                 sfor<CPT>([&](auto c_) {
@@ -590,6 +680,7 @@ __global__ void __launch_bounds__((NW + 1) * 32,
                 (void)NDN;
                 xslot ^= 1;
             }
+            if constexpr (MIRROR) vfix(std::true_type{});
             sfor<4>([&](auto c_) {
                 constexpr int C = decltype(c_)::value;
                 if constexpr (uses(U, C, -1, -1))
@@ -601,6 +692,7 @@ __global__ void __launch_bounds__((NW + 1) * 32,
                 if constexpr (uses(U, C, 1, 1))
                     sr[R + 1][C] = __shfl_down_sync(0xffffffffu, gd[0][C], 1);
             });
+            if constexpr (MIRROR) hfix(sl, sr, 0, R + 1);  // corners (and rows again)
             row(std::integral_constant<int, 0>{});
             row(std::integral_constant<int, R - 1>{});
 #pragma unroll
@@ -896,10 +988,36 @@ inline Plan plan_tiles(const WlLevel& L, int H, int R, int NW, int CPT) {
                             : (L.direction == 0 ? TWC - 2 * H : ((TWC - 2 * H) & ~3));
     const int TH = NW * R - 2 * H;
     const bool wide = CPT == 4;
-    const int X0 = wide ? (L.boundary == 0 || L.yhi > 0 ? 0 : HX) : H, Y0 = H + 1;
+    // Symmetric images whose width is a multiple of the lane width run the
+    // whole-image grid too: border tiles mirror their ghost cells per step
+    // (kernel `mtile`); otherwise only interior tiles run here and the frame
+    // goes to the interpreter.
+    bool full_sym = L.boundary == 1 && L.yhi == 0 && L.qw >= 2 && L.qh >= 2 &&
+                    L.qw % CPT == 0 && WL_SYM_FAST;
+    // Row offset of the symmetric grid: every tile whose compute rows hold
+    // image row 0 must not have it as a warp's last row (its mirror source,
+    // row 1, would sit in the next warp), nor row qh-1 as a warp's first row.
+    const int THs = NW * R - 2 * H;
+    auto rows_ok = [&](int y0) {
+        for (int ty = -1;; ++ty) {
+            const int c0 = y0 + ty * THs - H, c1 = c0 + NW * R;  // compute rows [c0, c1)
+            if (c0 > L.qh) return true;
+            if (c0 <= 0 && 0 < c1 && (0 - c0) % R == R - 1) return false;
+            if (c0 <= L.qh - 1 && L.qh - 1 < c1 && (L.qh - 1 - c0) % R == 0) return false;
+        }
+    };
+    int ysym = 0;
+    if (full_sym) {
+        for (int y0 = H + 1; y0 <= THs && !ysym; ++y0)
+            if (rows_ok(y0)) ysym = y0;
+        full_sym = ysym > 0;
+    }
+    const bool whole = L.boundary == 0 || L.yhi > 0 || full_sym;
+    const int X0 = wide ? (whole ? 0 : HX) : H, Y0 = full_sym ? ysym : H + 1;
     const int tx0 = wide ? 0 : -1;  // periodic plans
     int tx, ty;
     int y0 = Y0;
+    p.args.mirror = full_sym ? 1 : 0;
     if (L.yhi > 0) {
         if (L.boundary != 0 || L.ylo < H + 1 || L.yhi > L.qh - H - 1 || L.yhi <= L.ylo)
             return p;  // ok = false
@@ -911,12 +1029,12 @@ inline Plan plan_tiles(const WlLevel& L, int H, int R, int NW, int CPT) {
         p.args.wrap = 1;
         p.args.ylo = L.ylo;
         p.args.yhi = L.yhi;
-    } else if (L.boundary == 0) {
+    } else if (whole) {
         tx = (L.qw - X0 > 0 ? (L.qw - X0 + TW - 1) / TW : 0) - tx0;
         ty = (L.qh - Y0 > 0 ? (L.qh - Y0 + TH - 1) / TH : 0) + 1;
         p.args.tx0 = tx0;
         p.args.ty0 = -1;
-        p.args.wrap = 1;
+        p.args.wrap = full_sym ? 0 : 1;
     } else {
         const int c0 = X0 - HX;  // first compute column of tile 0 (>= 0)
         tx = L.qw - c0 >= TWC ? (L.qw - c0 - TWC) / TW + 1 : 0;
@@ -970,12 +1088,12 @@ cudaError_t launch(const WlLevel& L, const Plan& plan, cudaStream_t stream) {
     a.out_pitch = L.out_pitch;
     a.scaling = L.scaling && wl_host_program(L.prog).has_scale;
     a.scale = wl_host_program(L.prog).scale;
-    auto kern = fast_kernel<P, DIR, R, NW, CPT, NS, XF>;
-    static int max_blocks[64] = {};
     int dev = 0;
     cudaGetDevice(&dev);
-    int& mb = max_blocks[dev & 63];
-    if (mb == 0) {
+    // grid cap per kernel variant: persistent CTAs = SMs x resident CTAs
+    auto cap_of = [&](auto kern, int* cache) {
+        int& mb = cache[dev & 63];
+        if (mb != 0) return mb;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)G::kSmemBytes);
         int per_sm = 0;
@@ -983,15 +1101,30 @@ cudaError_t launch(const WlLevel& L, const Plan& plan, cudaStream_t stream) {
                                                       G::kSmemBytes);
         int sms = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        const int cap = MAXB;
-        if (cap > 0 && per_sm > cap) per_sm = cap;
+        if (MAXB > 0 && per_sm > MAXB) per_sm = MAXB;
         mb = (per_sm > 0 ? per_sm : 1) * sms;
-    }
-    const int grid = a.ntiles < mb ? a.ntiles : mb;
-    cudaError_t le = launch_pdl(kern, dim3(grid), dim3((NW + 1) * 32), G::kSmemBytes, stream,
-                                maps[0], maps[1], maps[2], maps[3], a);
-    wl_count_launch();
-    return le != cudaSuccess ? le : cudaGetLastError();
+        if (getenv("WL_VERBOSE"))
+            fprintf(stderr, "[wl] fast_kernel R=%d NW=%d CPT=%d NS=%d smem=%zu B: %d CTA/SM\n", R,
+                    NW, CPT, NS, (size_t)G::kSmemBytes, per_sm);
+        return mb;
+    };
+    static int cap_norm[64] = {}, cap_mirr[64] = {};
+    auto run = [&](auto kern, int* cache, int filter) -> cudaError_t {
+        const int mb = cap_of(kern, cache);
+        FastArgs f = a;
+        f.filter = filter;
+        const int grid = f.ntiles < mb ? f.ntiles : mb;
+        cudaError_t le = launch_pdl(kern, dim3(grid), dim3((NW + 1) * 32), G::kSmemBytes,
+                                    stream, maps[0], maps[1], maps[2], maps[3], f);
+        wl_count_launch();
+        return le != cudaSuccess ? le : cudaGetLastError();
+    };
+    if (!a.mirror) return run(fast_kernel<P, DIR, R, NW, CPT, NS, XF, false>, cap_norm, 0);
+    // symmetric whole-image plan: interior tiles on the plain kernel, the ring
+    // of border tiles on the mirroring variant (same grid, disjoint tiles)
+    cudaError_t e = run(fast_kernel<P, DIR, R, NW, CPT, NS, XF, false>, cap_norm, 1);
+    if (e != cudaSuccess) return e;
+    return run(fast_kernel<P, DIR, R, NW, CPT, NS, XF, true>, cap_mirr, 2);
 }
 
 }  // namespace wlfast

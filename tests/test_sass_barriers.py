@@ -19,15 +19,18 @@ CUOBJDUMP = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
 
 
 def barrier_counts(lib_path):
+    """{(wavelet, scheme, dir, mangled name): BAR count} for every fast
+    kernel -- each program has a plain and a symmetric-border (mirroring)
+    instantiation, checked separately."""
     out = subprocess.run([CUOBJDUMP, "-sass", lib_path], capture_output=True, text=True,
                          check=True).stdout
     counts, fn = {}, None
     for line in out.splitlines():
         m = re.search(r"Function : (\S+)", line)
         if m:
-            fn = m.group(1)
-            km = re.search(r"fast_kernelI\d+P_(cdf\d+)_(\w+?)_(fwd|inv)", fn)
-            fn = km.groups() if km else None
+            name = m.group(1)
+            km = re.search(r"fast_kernelI\d+P_(cdf\d+)_(\w+?)_(fwd|inv)", name)
+            fn = km.groups() + (name,) if km else None
             if fn:
                 counts.setdefault(fn, 0)
             continue
@@ -39,8 +42,10 @@ def barrier_counts(lib_path):
 @pytest.mark.skipif(not os.path.exists(CUOBJDUMP), reason="cuobjdump not available")
 def test_sass_barriers_equal_count_barriers():
     counts = barrier_counts(wl.LIB_PATH)
-    assert len(counts) == 2 * 9 * 2, sorted(counts)
-    for (w, s, d), n in counts.items():
+    programs = {k[:3] for k in counts}
+    assert len(programs) == 2 * 9 * 2, sorted(programs)
+    assert len(counts) == 2 * len(programs)  # plain + mirroring variant
+    for (w, s, d, _), n in counts.items():
         want = wl.build_scheme(s, w).info(0 if d == "fwd" else 1)["barriers"]
         assert n == want, (w, s, d, n, want)
 
@@ -56,7 +61,7 @@ def build_broken(epoch=1):
 def test_broken_barrier_variant_drops_one_barrier():
     lib = build_broken(1)
     counts = barrier_counts(lib)
-    for (w, s, d), n in counts.items():
+    for (w, s, d, _), n in counts.items():
         want = wl.build_scheme(s, w).info(0 if d == "fwd" else 1)["barriers"]
         # epoch 1 exists only for schemes with >= 2 barriers
         assert n == (want - 1 if want >= 2 else want), (w, s, d, n, want)

@@ -12,7 +12,8 @@ wl.set_engine(2)  # fast engine only: the kernels with the per-epoch barriers
 img = torch.rand((96, 512), device="cuda")
 for w, s in (("cdf53", "sweldens"), ("cdf97", "monolithic_star")):
     sch = wl.build_scheme(s, w)
-    q = wl.forward(img, sch)
-    wl.inverse(q, w, scheme=s)
+    for b in ("periodic", "symmetric"):  # symmetric: interior + mirroring border kernels
+        q = wl.forward(img, sch, b)
+        wl.inverse(q, w, b, scheme=s)
 torch.cuda.synchronize()
 print("workload done")
