@@ -5,8 +5,9 @@
 // Large periodic cdf53/cdf97 transforms are pipelined in row chunks: chunk k
 // is copied host->device (with the halo rows the strip transform needs,
 // wrapped at the image border), transformed by the strip kernels
-// (bit-identical rows of the whole-image transform) and copied back, on one
-// of three streams, so PCIe in both directions and the kernels overlap. Every
+// (bit-identical rows of the whole-image transform) and copied back -- one
+// stream per copy direction plus one for the kernels, chained by events per
+// buffer slot, so PCIe in both directions and the kernels overlap. Every
 // other case (symmetric boundary, dd137, small or unaligned images) runs
 // whole-image: copy in, transform, copy out. The call returns when the
 // result is in host memory. Host buffers should be pinned
@@ -23,15 +24,27 @@
 
 namespace {
 
-constexpr int kSlots = 3;
+constexpr int kMaxSlots = 8;
+// pipeline depth (streams / device buffers); WL_HOST_SLOTS overrides (tuning)
+int slots() {
+    static const int v = [] {
+        const char* e = getenv("WL_HOST_SLOTS");
+        const int n = e ? atoi(e) : 3;
+        return n < 2 ? 2 : (n > kMaxSlots ? kMaxSlots : n);
+    }();
+    return v;
+}
 constexpr size_t kChunkBytes = 32u << 20;  // target input bytes per chunk
 
 struct Workspace {
     int device = -1;
-    cudaStream_t streams[kSlots] = {};
-    cudaEvent_t done[kSlots] = {};
-    float* in[kSlots] = {};
-    float* out[kSlots] = {};
+    cudaStream_t streams[kMaxSlots] = {};
+    cudaEvent_t done[kMaxSlots] = {};
+    // chunk pipeline: one stream per copy direction and one for kernels
+    // (streams[0..2]), chained per buffer slot by events
+    cudaEvent_t h2d_done[kMaxSlots] = {}, k_done[kMaxSlots] = {}, d2h_done[kMaxSlots] = {};
+    float* in[kMaxSlots] = {};
+    float* out[kMaxSlots] = {};
     size_t in_cap = 0, out_cap = 0;  // floats per slot
 
     bool ensure(size_t in_floats, size_t out_floats) {
@@ -40,22 +53,25 @@ struct Workspace {
         if (device != dev) {
             release();
             device = dev;
-            for (int s = 0; s < kSlots; ++s) {
+            for (int s = 0; s < kMaxSlots; ++s) {
                 if (cudaStreamCreateWithFlags(&streams[s], cudaStreamNonBlocking) != cudaSuccess)
                     return false;
-                if (cudaEventCreateWithFlags(&done[s], cudaEventDisableTiming) != cudaSuccess)
+                if (cudaEventCreateWithFlags(&done[s], cudaEventDisableTiming) != cudaSuccess ||
+                    cudaEventCreateWithFlags(&h2d_done[s], cudaEventDisableTiming) != cudaSuccess ||
+                    cudaEventCreateWithFlags(&k_done[s], cudaEventDisableTiming) != cudaSuccess ||
+                    cudaEventCreateWithFlags(&d2h_done[s], cudaEventDisableTiming) != cudaSuccess)
                     return false;
             }
         }
         if (in_floats > in_cap || out_floats > out_cap) {
-            for (int s = 0; s < kSlots; ++s) {
+            for (int s = 0; s < kMaxSlots; ++s) {
                 cudaFree(in[s]);
                 cudaFree(out[s]);
                 in[s] = out[s] = nullptr;
             }
             in_cap = in_floats > in_cap ? in_floats : in_cap;
             out_cap = out_floats > out_cap ? out_floats : out_cap;
-            for (int s = 0; s < kSlots; ++s) {
+            for (int s = 0; s < slots(); ++s) {
                 if (cudaMalloc(&in[s], in_cap * sizeof(float)) != cudaSuccess) return false;
                 if (cudaMalloc(&out[s], out_cap * sizeof(float)) != cudaSuccess) return false;
             }
@@ -64,11 +80,13 @@ struct Workspace {
     }
     void release() {
         if (device < 0) return;
-        for (int s = 0; s < kSlots; ++s) {
+        for (int s = 0; s < kMaxSlots; ++s) {
             cudaFree(in[s]);
             cudaFree(out[s]);
             if (streams[s]) cudaStreamDestroy(streams[s]);
             if (done[s]) cudaEventDestroy(done[s]);
+            for (cudaEvent_t* ev : {&h2d_done[s], &k_done[s], &d2h_done[s]})
+                if (*ev) cudaEventDestroy(*ev), *ev = nullptr;
             in[s] = out[s] = nullptr;
             streams[s] = nullptr;
             done[s] = nullptr;
@@ -161,6 +179,30 @@ std::vector<int> chunk_plan(int total, int R, int align) {
     return out;
 }
 
+// One chunk through the pipeline on buffer slot s: H2D on the copy-in
+// stream (after the kernel that last read in[s]), the kernel on the compute
+// stream (after this H2D and after the D2H that last read out[s]), the D2H
+// on the copy-out stream. Each copy engine sees only its own direction.
+template <class H, class K, class D>
+int pipe_chunk(int s, H&& h2d, K&& ker, D&& d2h) {
+    Workspace& w = g_ws;
+    cudaStream_t si = w.streams[0], sk = w.streams[1], so = w.streams[2];
+    cudaStreamWaitEvent(si, w.k_done[s], 0);
+    cudaError_t e = h2d(si);
+    if (e != cudaSuccess) return cuda_err(e, "H2D");
+    cudaEventRecord(w.h2d_done[s], si);
+    cudaStreamWaitEvent(sk, w.h2d_done[s], 0);
+    cudaStreamWaitEvent(sk, w.d2h_done[s], 0);
+    const int r = ker(sk);
+    if (r != WL_OK) return r;
+    cudaEventRecord(w.k_done[s], sk);
+    cudaStreamWaitEvent(so, w.k_done[s], 0);
+    e = d2h(so);
+    if (e != cudaSuccess) return cuda_err(e, "D2H");
+    cudaEventRecord(w.d2h_done[s], so);
+    return WL_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -207,29 +249,34 @@ int wl_dwt2_forward_host(const float* img, int w, int h, long img_pitch, int wav
     const std::vector<int> plan = chunk_plan(h, R, 2);
     int r0 = 0;
     for (size_t k = 0; k < plan.size(); r0 += plan[k], ++k) {
-        const int s = k % kSlots;
-        cudaStream_t st = g_ws.streams[s];
+        const int s = static_cast<int>(k % slots());
         const int rows = plan[k];
         const int r1 = r0 + rows;
-        cudaError_t e = rows_h2d(g_ws.in[s], w, img, img_pitch, w, h, r0 - halo, r1 + halo, st);
-        if (e != cudaSuccess) return cuda_err(e, "H2D");
         float* o = g_ws.out[s];
         const size_t npc = static_cast<size_t>(qw) * (rows / 2);
-        const int r = wl_dwt2_forward_strip(g_ws.in[s] + static_cast<size_t>(halo) * w, w, rows,
-                                            halo, w, wavelet, scheme, scaling, o, o + npc,
-                                            o + 2 * npc, o + 3 * npc, qw, st);
+        const int r = pipe_chunk(
+            s,
+            [&](cudaStream_t st) {
+                return rows_h2d(g_ws.in[s], w, img, img_pitch, w, h, r0 - halo, r1 + halo, st);
+            },
+            [&](cudaStream_t st) {
+                return wl_dwt2_forward_strip(g_ws.in[s] + static_cast<size_t>(halo) * w, w,
+                                             rows, halo, w, wavelet, scheme, scaling, o, o + npc,
+                                             o + 2 * npc, o + 3 * npc, qw, st);
+            },
+            [&](cudaStream_t st) {
+                for (int c = 0; c < 4; ++c) {
+                    const cudaError_t e =
+                        copy_rows(hp[c] + static_cast<long>(r0 / 2) * plane_pitch, plane_pitch,
+                                  o + c * npc, qw, qw, rows / 2, cudaMemcpyDeviceToHost, st);
+                    if (e != cudaSuccess) return e;
+                }
+                return cudaSuccess;
+            });
         if (r != WL_OK) return r;
-        for (int c = 0; c < 4; ++c) {
-            e = copy_rows(hp[c] + static_cast<long>(r0 / 2) * plane_pitch, plane_pitch,
-                          o + c * npc, qw, qw, rows / 2, cudaMemcpyDeviceToHost, st);
-            if (e != cudaSuccess) return cuda_err(e, "D2H");
-        }
     }
-    for (int s = 0; s < kSlots; ++s) {
-        cudaError_t e = cudaStreamSynchronize(g_ws.streams[s]);
-        if (e != cudaSuccess) return cuda_err(e, "forward_host");
-    }
-    return WL_OK;
+    const cudaError_t e = cudaStreamSynchronize(g_ws.streams[2]);  // last D2H waits on all
+    return e == cudaSuccess ? WL_OK : cuda_err(e, "forward_host");
 }
 
 int wl_dwt2_inverse_host(const float* ll, const float* hl, const float* lh, const float* hh,
@@ -271,31 +318,35 @@ int wl_dwt2_inverse_host(const float* ll, const float* hl, const float* lh, cons
     const std::vector<int> plan = chunk_plan(qh, R, 1);
     int q0 = 0;
     for (size_t k = 0; k < plan.size(); q0 += plan[k], ++k) {
-        const int s = k % kSlots;
-        cudaStream_t st = g_ws.streams[s];
+        const int s = static_cast<int>(k % slots());
         const int rows = plan[k];
         const int q1 = q0 + rows;
         const size_t pb = static_cast<size_t>(qw) * (rows + 2 * halo);
-        for (int c = 0; c < 4; ++c) {
-            cudaError_t e = rows_h2d(g_ws.in[s] + c * pb, qw, hp[c], plane_pitch, qw, qh,
-                                     q0 - halo, q1 + halo, st);
-            if (e != cudaSuccess) return cuda_err(e, "H2D");
-        }
         float* d = g_ws.in[s] + static_cast<size_t>(halo) * qw;
-        const int r = wl_dwt2_inverse_strip(d, d + pb, d + 2 * pb, d + 3 * pb, qw, rows, halo, qw,
-                                            wavelet, scheme, undo_scaling, g_ws.out[s], 2 * qw,
-                                            st);
+        const int r = pipe_chunk(
+            s,
+            [&](cudaStream_t st) {
+                for (int c = 0; c < 4; ++c) {
+                    const cudaError_t e = rows_h2d(g_ws.in[s] + c * pb, qw, hp[c], plane_pitch, qw,
+                                                   qh, q0 - halo, q1 + halo, st);
+                    if (e != cudaSuccess) return e;
+                }
+                return cudaSuccess;
+            },
+            [&](cudaStream_t st) {
+                return wl_dwt2_inverse_strip(d, d + pb, d + 2 * pb, d + 3 * pb, qw, rows, halo,
+                                             qw, wavelet, scheme, undo_scaling, g_ws.out[s],
+                                             2 * qw, st);
+            },
+            [&](cudaStream_t st) {
+                return copy_rows(img + static_cast<long>(2 * q0) * img_pitch, img_pitch,
+                                 g_ws.out[s], 2 * qw, 2 * qw, 2 * rows, cudaMemcpyDeviceToHost,
+                                 st);
+            });
         if (r != WL_OK) return r;
-        cudaError_t e = copy_rows(img + static_cast<long>(2 * q0) * img_pitch, img_pitch,
-                                  g_ws.out[s], 2 * qw, 2 * qw, 2 * rows, cudaMemcpyDeviceToHost,
-                                  st);
-        if (e != cudaSuccess) return cuda_err(e, "D2H");
     }
-    for (int s = 0; s < kSlots; ++s) {
-        cudaError_t e = cudaStreamSynchronize(g_ws.streams[s]);
-        if (e != cudaSuccess) return cuda_err(e, "inverse_host");
-    }
-    return WL_OK;
+    const cudaError_t e = cudaStreamSynchronize(g_ws.streams[2]);  // last D2H waits on all
+    return e == cudaSuccess ? WL_OK : cuda_err(e, "inverse_host");
 }
 
 }  // extern "C"
