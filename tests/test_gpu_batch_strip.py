@@ -291,3 +291,21 @@ def test_batch_pyramid_large(wl):
             assert torch.equal(pyrs[i], wl.multi_level_forward(imgs[i], sch, 3).flat), (w, i)
         rec = wl.multi_level_inverse_batch(pyrs, 4096, 4096, 3, w, scheme="monolithic_star")
         assert (rec - imgs).abs().max().item() <= 3e-5
+
+
+def test_batch_beyond_int32_elements(wl):
+    """Maximum sizes: one batched launch over 132 x 4096^2 images (2.2e9
+    elements > 2^31): 64-bit image offsets in the kernels and 3-D TMA maps.
+    The last images equal their single-image pyramids bit for bit."""
+    import torch
+    n = 132
+    imgs = torch.empty((n, 4096, 4096), device="cuda")
+    imgs[:-2].fill_(0.25)
+    imgs[-2:] = rand((2, 4096, 4096), 35)
+    sch = wl.build_scheme("monolithic_star", "cdf97")
+    pyrs = wl.multi_level_forward_batch(imgs, sch, 2)
+    for i in (n - 2, n - 1):
+        assert torch.equal(pyrs[i], wl.multi_level_forward(imgs[i], sch, 2).flat), i
+    assert torch.all(pyrs[0, -1024 * 1024:] == pyrs[0, -1]).item()  # constant image: flat LL
+    del imgs, pyrs
+    torch.cuda.empty_cache()
