@@ -927,9 +927,15 @@ struct Config<1, 1> {  // cdf97 inverse
 template <int WAVELET, int DIR, int SCHEME>
 struct SchemeConfig : Config<WAVELET, DIR> {};
 #if WL_POLY_INV_CPT4
+#ifndef WL_POLY_R
+#define WL_POLY_R 3
+#endif
+#ifndef WL_POLY_NW
+#define WL_POLY_NW 10
+#endif
 template <int SCHEME>
 struct PolyInv {
-    static constexpr int R = 4, NW = 8, CPT = 4, NS = 2;
+    static constexpr int R = WL_POLY_R, NW = WL_POLY_NW, CPT = 4, NS = 2;
     static constexpr bool XF = false;
     static constexpr int MAXB = 0;
 };
@@ -942,7 +948,8 @@ struct SchemeConfig<1, 1, 7> : PolyInv<7> {};  // cdf97 polyphase inverse
 template <>
 struct SchemeConfig<1, 0, 7> : Config<1, 0> {
     static constexpr int NS = 2;
-    static constexpr int R = 4;  // 40-row tiles measured slower for Polyphase
+    static constexpr int R = WL_POLY_R;  // 30-row tiles x 10 warps (profiles/tuning_r01_poly.txt)
+    static constexpr int NW = WL_POLY_NW;
 };
 
 // cdf97 Monolithic / Monolithic* inverses: full exchange measured faster
