@@ -18,7 +18,13 @@
 
 namespace {
 
-constexpr int TQX = 64, TQY = 32, Q = 4, NT = 256;
+#ifndef WL_CONV_Q
+#define WL_CONV_Q 4
+#endif
+#ifndef WL_CONV_TQY
+#define WL_CONV_TQY 32
+#endif
+constexpr int TQX = 64, TQY = WL_CONV_TQY, Q = WL_CONV_Q, NT = 256;
 constexpr int MARGIN = 4;                 // staged pixel columns left of the tile
 constexpr int SW = 2 * TQX + 2 * MARGIN;  // staged row length (136 px)
 
@@ -129,8 +135,11 @@ __global__ void __launch_bounds__(NT) conv_fast_kernel(const __grid_constant__ C
         for (int c = 0; c < 4; ++c) {
             float* p = a.out[c] + b * a.out_bstride[c] + off;
             if (a.vec4 && gx + Q <= a.qw) {
-                *reinterpret_cast<float4*>(p) =
-                    make_float4(acc[0][c], acc[1][c], acc[2][c], acc[3][c]);
+                static_assert(Q % 4 == 0, "float4 stores of Q quads");
+#pragma unroll
+                for (int q = 0; q < Q; q += 4)
+                    *reinterpret_cast<float4*>(p + q) =
+                        make_float4(acc[q][c], acc[q + 1][c], acc[q + 2][c], acc[q + 3][c]);
             } else {
 #pragma unroll
                 for (int q = 0; q < Q; ++q)
