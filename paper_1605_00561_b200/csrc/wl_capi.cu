@@ -276,6 +276,20 @@ int wl_strip_halo_rows(int wavelet, int scheme, int direction) {
 int wl_dwt2_forward_strip(const float* strip, int w, int rows, int halo_rows, long pitch,
                           int wavelet, int scheme, int scaling, float* ll, float* hl, float* lh,
                           float* hh, long plane_pitch, void* stream) {
+    return wl_forward_strip_wait(strip, w, rows, halo_rows, pitch, wavelet, scheme, scaling, ll,
+                                 hl, lh, hh, plane_pitch, stream, nullptr, nullptr, 0, nullptr);
+}
+
+}  // extern "C"
+
+bool wl_strip_wait_capable(int wavelet, int scheme) {
+    return !wl_host_program(prog_index(wavelet, scheme, 0)).is_conv;
+}
+
+int wl_forward_strip_wait(const float* strip, int w, int rows, int halo_rows, long pitch,
+                          int wavelet, int scheme, int scaling, float* ll, float* hl, float* lh,
+                          float* hh, long plane_pitch, void* stream, const unsigned* xflag_a,
+                          const unsigned* xflag_b, unsigned xepoch, unsigned* xerr) {
     if (w <= 0 || rows <= 0 || w % 2 != 0 || rows % 2 != 0)
         return fail(WL_EINVAL, "forward requires even positive dimensions");
     if (!valid_ids(wavelet, scheme, 0) || wavelet > WL_CDF97)
@@ -302,13 +316,22 @@ int wl_dwt2_forward_strip(const float* strip, int w, int rows, int halo_rows, lo
     L.scaling = scaling != 0;
     L.ylo = halo_rows / 2;
     L.yhi = L.ylo + rows / 2;
+    L.xflag_a = xflag_a;
+    L.xflag_b = xflag_b;
+    L.xepoch = xepoch;
+    L.xerr = xerr;
     const WlProgram& P = wl_host_program(L.prog);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    if (P.is_conv) return cuda_status(wl_launch_conv_fast(L, s), "conv_kernel");
+    if (P.is_conv) {
+        if (xflag_a) return fail(WL_EINVAL, "halo wait needs a lifting scheme");
+        return cuda_status(wl_launch_conv_fast(L, s), "conv_kernel");
+    }
     if (!wl_fast_supported(L))
         return fail(WL_EINVAL, "strip transform needs 16-byte aligned buffers and pitches");
     return cuda_status(wl_launch_fast(L, s), "fast_kernel");
 }
+
+extern "C" {
 
 int wl_dwt2_inverse_strip(const float* ll, const float* hl, const float* lh, const float* hh,
                           int qw, int qrows, int halo_qrows, long plane_pitch, int wavelet,

@@ -218,7 +218,46 @@ struct FastArgs {
     int ylo, yhi;        // stored cell rows [ylo, yhi); out[] addresses row ylo
     int mirror;          // symmetric plan covering the whole image (border tiles mirror)
     int filter;          // 0 every tile, 1 interior tiles only, 2 border tiles only
+    // strip halo wait (WlLevel::xflag_a): edge tile rows last, producer waits
+    const unsigned* xflag_a;
+    const unsigned* xflag_b;
+    unsigned xepoch;
+    unsigned* xerr;
 };
+
+// Tile-row order: with a halo wait the window's first and last tile rows go
+// last (sequence k -> row: 1..n-2, 0, n-1), so the wait overlaps the
+// interior tiles. (Row n-2 can also reach the lower halo when the last row
+// is short; it then simply waits a little earlier.)
+__device__ __forceinline__ int tile_row_of(int k, int n, bool edge_last) {
+    if (!edge_last || n <= 2) return k;
+    return k < n - 2 ? k + 1 : (k == n - 2 ? 0 : n - 1);
+}
+
+// System-scope acquire spin on two flags (halo pushed by neighbour ranks),
+// bounded by a 10 s timeout that sets *err.
+__device__ __forceinline__ unsigned ld_acquire_sys_u32(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ inline void wait_halo_flags(const unsigned* fa, const unsigned* fb, unsigned e,
+                                       unsigned* err) {
+    unsigned long long t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    unsigned ns = 64;
+    while ((int)(ld_acquire_sys_u32(fa) - e) < 0 || (int)(ld_acquire_sys_u32(fb) - e) < 0) {
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (t - t0 > 10ull * 1000 * 1000 * 1000) {
+            atomicExch(err, 1u);
+            return;
+        }
+        __nanosleep(ns);
+        ns = ns < 1024 ? 2 * ns : 1024;
+    }
+    // the halo rows will be read by TMA (async proxy) and generic loads
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+}
 
 template <int R, int NW, int CPT, int NS = 2, int NXC = 4>
 struct Geometry {
@@ -343,6 +382,7 @@ __global__ void __launch_bounds__((NW + 1) * 32,
     if (warp == NW) {
         // ---------------- producer warp: TMA tile stream ----------------
         if (lane == 0) {
+            bool halo_ready = false;
             for (int i = 0, t = blockIdx.x; t < a.ntiles; t += gridDim.x) {
                 if (a.filter) {  // interior-only / border-only launch of a symmetric plan
                     const int fb = t / a.ntiles_img, ft = t - fb * a.ntiles_img;
@@ -364,10 +404,16 @@ __global__ void __launch_bounds__((NW + 1) * 32,
 #endif
                 }
                 const int b = t / a.ntiles_img, tt = t - b * a.ntiles_img;
-                const int tyi = tt / a.tiles_x;
-                const int ty = tyi + a.ty0, tx = tt - tyi * a.tiles_x + a.tx0;
+                const int ntr = a.ntiles_img / a.tiles_x;
+                const int tyk = tt / a.tiles_x;
+                const int tyi = tile_row_of(tyk, ntr, a.xflag_a != nullptr);
+                const int ty = tyi + a.ty0, tx = tt - tyk * a.tiles_x + a.tx0;
                 const int cx = a.X0 + tx * a.TW - HX;     // first compute cell column
                 const int cy = a.Y0 + ty * a.TH - H - 1;  // ghost row above the region
+                if (a.xflag_a && !halo_ready && (cy < a.ylo || cy + G::kRows > a.yhi)) {
+                    wait_halo_flags(a.xflag_a, a.xflag_b, a.xepoch, a.xerr);
+                    halo_ready = true;
+                }
                 float* dst = stage + s * G::kStageFloats;
                 mbar_expect_tx(&full[s], G::kStageBytes);
                 if (DIR == 0) {
@@ -397,8 +443,9 @@ __global__ void __launch_bounds__((NW + 1) * 32,
     for (int i = 0, t = blockIdx.x; t < a.ntiles; t += gridDim.x) {
         const int s = i % NS;
         const int b = t / a.ntiles_img, tt = t - b * a.ntiles_img;
-        const int tyi = tt / a.tiles_x;
-        const int ty = tyi + a.ty0, tx = tt - tyi * a.tiles_x + a.tx0;
+        const int tyk = tt / a.tiles_x;
+        const int tyi = tile_row_of(tyk, a.ntiles_img / a.tiles_x, a.xflag_a != nullptr);
+        const int ty = tyi + a.ty0, tx = tt - tyk * a.tiles_x + a.tx0;
         const int cx = a.X0 + tx * a.TW - HX;     // first compute cell column
         const int cy = a.Y0 + ty * a.TH - H - 1;  // ghost row above the region
         // Border tile: its compute region leaves the image. Periodic plans
@@ -1091,6 +1138,10 @@ cudaError_t launch(const WlLevel& L, const Plan& plan, cudaStream_t stream) {
         a.out[1] = a.out[2] = a.out[3] = nullptr;
     }
     for (int k = 0; k < 4; ++k) a.in[k] = L.in[k];
+    a.xflag_a = L.xflag_a;
+    a.xflag_b = L.xflag_b;
+    a.xepoch = L.xepoch;
+    a.xerr = L.xerr;
     a.in_pitch = L.in_pitch;
     a.out_pitch = L.out_pitch;
     a.scaling = L.scaling && wl_host_program(L.prog).has_scale;

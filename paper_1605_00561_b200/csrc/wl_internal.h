@@ -25,6 +25,15 @@ struct WlLevel {
     // [ylo, yhi) of the qh-row buffer are produced; out[] points at row ylo.
     // yhi == 0: the whole plane (out[] at row 0).
     int ylo, yhi;
+    // Strip-pyramid halo wait (wl_strips.cu): when xflag_a is set, the fast
+    // engine schedules the window's first and last tile rows last and its
+    // producer waits until *xflag_a and *xflag_b reach xepoch (system-scope
+    // acquire, timeout -> *xerr) before loading them -- the only tiles that
+    // read the halo rows pushed by the neighbour ranks.
+    const unsigned* xflag_a;
+    const unsigned* xflag_b;
+    unsigned xepoch;
+    unsigned* xerr;
 };
 
 const WlProgram& wl_host_program(int prog);
@@ -53,3 +62,11 @@ bool wl_fast_supported(const WlLevel& L);
 void wl_count_launch();
 // Records `msg` as this thread's wl_last_error() and returns `code`.
 int wl_fail(int code, const char* msg);
+
+// Strip forward with the halo wait folded into the fast engine (wl_strips.cu):
+// identical to wl_dwt2_forward_strip, plus WlLevel::xflag_* (null = no wait).
+bool wl_strip_wait_capable(int wavelet, int scheme);
+int wl_forward_strip_wait(const float* strip, int w, int rows, int halo_rows, long pitch,
+                          int wavelet, int scheme, int scaling, float* ll, float* hl, float* lh,
+                          float* hh, long plane_pitch, void* stream, const unsigned* xflag_a,
+                          const unsigned* xflag_b, unsigned xepoch, unsigned* xerr);

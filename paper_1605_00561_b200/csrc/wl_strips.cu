@@ -22,16 +22,22 @@
 //   for l in 0..L-1:
 //   1. exchange kernel: copy the top/bottom `halo` interior rows of level l
 //      into the up/down neighbour's halo rows; the last CTA to finish fences
-//      (system scope), release-stores e into the neighbours' flags, then
-//      spins (acquire, bounded by a timeout) until both of its own flags for
-//      level l reached e;
-//   2. strip transform of level l.
+//      (system scope) and release-stores e into the neighbours' flags;
+//   2. strip transform of level l. Its producer warp spins (acquire, bounded
+//      by a timeout) until both of this rank's flags for level l reached e,
+//      but only right before the first tile that reads a halo row; those
+//      tile rows are scheduled last, so the wait overlaps the interior
+//      tiles (lifting schemes, neighbours on other GPUs; otherwise -- the
+//      Convolution kernel has no producer warp, and a neighbour sharing
+//      this GPU could need SM room the waiting grid holds -- the exchange
+//      kernel's last CTA does the wait, before the transform starts).
 //   3. signal done = e to both neighbours.
 // Periodic ring: rank 0's up neighbour is rank G-1. With one rank the
 // neighbour is the rank itself (the wrap copies within its own buffer).
 #include <unistd.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -50,6 +56,7 @@ struct Blob {  // IPC export of a rank's window (fits WL_STRIPS_BLOB_BYTES)
     int device;
     unsigned long long ptr;  // window address in the exporting process
     unsigned long long bytes;
+    unsigned char uuid[16];  // GPU identity, independent of CUDA_VISIBLE_DEVICES
 };
 
 __device__ __forceinline__ void st_release_sys(unsigned* p, unsigned v) {
@@ -94,6 +101,7 @@ struct XchArgs {
     unsigned* counter;  // CTA completion counter (my window)
     unsigned* err;      // host-mapped error word
     int vec4;
+    int wait;           // 1: last CTA also waits for my halos (else the transform does)
 };
 
 __global__ void __launch_bounds__(256) exchange_kernel(const XchArgs a) {
@@ -121,7 +129,7 @@ __global__ void __launch_bounds__(256) exchange_kernel(const XchArgs a) {
             __threadfence_system();
             st_release_sys(a.sig_up, a.epoch);
             st_release_sys(a.sig_down, a.epoch);
-            wait_flags(a.my_a, a.my_b, a.epoch, a.err);
+            if (a.wait) wait_flags(a.my_a, a.my_b, a.epoch, a.err);
         }
     }
 }
@@ -149,6 +157,8 @@ struct WlStrips {
     char* up = nullptr;          // neighbours' windows (mapped)
     char* down = nullptr;
     bool up_opened = false, down_opened = false;
+    bool peer_same_device = false;  // a neighbour rank (not me) lives on my GPU
+    unsigned char uuid[16] = {};
     unsigned* err_host = nullptr;  // host-mapped
     unsigned* err_dev = nullptr;
     unsigned epoch = 0;
@@ -199,6 +209,11 @@ int wl_strips_create(int w, int h, int rank, int nranks, int levels, int wavelet
     s->nranks = nranks;
     s->halo = halo;
     cudaGetDevice(&s->device);
+    {
+        cudaDeviceProp prop;
+        if (cudaGetDeviceProperties(&prop, s->device) == cudaSuccess)
+            memcpy(s->uuid, &prop.uuid, sizeof(s->uuid));
+    }
     size_t off = 0;
     for (int l = 0; l < levels; ++l) {
         s->lvl_off[l] = off;
@@ -254,6 +269,7 @@ int wl_strips_create(int w, int h, int rank, int nranks, int levels, int wavelet
             a.epoch = 0;
             a.counter = f + 2 * levels + 2;
             a.err = s->err_dev;
+            a.wait = 1;
             exchange_kernel<<<1, 256>>>(a);
             signal_kernel<<<1, 1>>>(f + 2 * levels + 3, f + 2 * levels + 4, 0);
             wait_kernel<<<1, 1>>>(f + 2 * levels + 3, f + 2 * levels + 4, 0, s->err_dev);
@@ -284,6 +300,7 @@ int wl_strips_export(WlStrips* s, void* blob) {
     b.device = s->device;
     b.ptr = reinterpret_cast<unsigned long long>(s->window);
     b.bytes = s->bytes;
+    memcpy(b.uuid, s->uuid, sizeof(b.uuid));
     memcpy(blob, &b, sizeof(b));
     return WL_OK;
 }
@@ -319,6 +336,13 @@ int wl_strips_connect(WlStrips* s, const void* up_blob, const void* down_blob) {
     memcpy(&d, down_blob, sizeof(d));
     int st = map_blob(s, u, nullptr, nullptr, &s->up, &s->up_opened);
     if (st != WL_OK) return st;
+    const unsigned long long me = reinterpret_cast<unsigned long long>(s->window);
+    const int mypid = static_cast<int>(getpid());
+    auto shares = [&](const Blob& b) {
+        const bool self = b.pid == mypid && b.ptr == me;
+        return !self && memcmp(b.uuid, s->uuid, sizeof(b.uuid)) == 0;
+    };
+    s->peer_same_device = shares(u) || shares(d);
     return map_blob(s, d, &u, s->up, &s->down, &s->down_opened);
 }
 
@@ -339,6 +363,20 @@ int wl_strips_forward(WlStrips* s, float* slice, void* stream) {
     unsigned* fu = s->flags(s->up);
     unsigned* fd = s->flags(s->down);
     const unsigned e = ++s->epoch;
+    // Lifting schemes: the exchange kernel only pushes and signals; the
+    // strip transform's producer waits for the neighbours' halos right before
+    // the tile rows that read them, which it schedules last (wl_fast_impl.cuh
+    // tile_row_of), so the wait hides behind the interior tiles.
+    // Only when no neighbour shares this GPU (or nranks == 1, where my own
+    // exchange precedes the transform on the stream): a neighbour on the
+    // same device could otherwise need SM room the waiting grid holds.
+    // WL_STRIP_OVERLAP=0 disables it, =2 forces it (single-GPU tests).
+    static const int overlap_env = [] {
+        const char* v = getenv("WL_STRIP_OVERLAP");
+        return v ? atoi(v) : 1;
+    }();
+    const bool overlap = wl_strip_wait_capable(s->wavelet, s->scheme) &&
+                         (overlap_env == 2 || (overlap_env == 1 && !s->peer_same_device));
     if (e > 1) {  // neighbours finished reading the halos of call e-1
         wait_kernel<<<1, 1, 0, st>>>(my + 2 * L, my + 2 * L + 1, e - 1, s->err_dev);
         wl_count_launch();
@@ -362,6 +400,7 @@ int wl_strips_forward(WlStrips* s, float* slice, void* stream) {
         a.counter = my + 2 * L + 2;
         a.err = s->err_dev;
         a.vec4 = (wl_ % 4) == 0;
+        a.wait = overlap ? 0 : 1;
         const long work = a.vec4 ? a.n / 4 : a.n;
         int blocks = static_cast<int>((work + 255) / 256);
         blocks = blocks < 1 ? 1 : (blocks > 148 ? 148 : blocks);
@@ -377,8 +416,10 @@ int wl_strips_forward(WlStrips* s, float* slice, void* stream) {
         off += 3 * np;
         float* ll = (l + 1 == L) ? slice + off
                                  : s->lvl(s->window, l + 1) + static_cast<size_t>(halo) * qw;
-        const int r = wl_dwt2_forward_strip(interior, wl_, sl_, halo, wl_, s->wavelet, s->scheme,
-                                            s->scaling, ll, hl, hl + np, hl + 2 * np, qw, stream);
+        const int r = wl_forward_strip_wait(
+            interior, wl_, sl_, halo, wl_, s->wavelet, s->scheme, s->scaling, ll, hl, hl + np,
+            hl + 2 * np, qw, stream, overlap ? my + 2 * l : nullptr,
+            overlap ? my + 2 * l + 1 : nullptr, e, s->err_dev);
         if (r != WL_OK) return r;
     }
     signal_kernel<<<1, 1, 0, st>>>(fu + 2 * L + 1, fd + 2 * L, e);

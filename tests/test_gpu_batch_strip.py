@@ -309,3 +309,26 @@ def test_batch_beyond_int32_elements(wl):
     assert torch.all(pyrs[0, -1024 * 1024:] == pyrs[0, -1]).item()  # constant image: flat LL
     del imgs, pyrs
     torch.cuda.empty_cache()
+
+
+def test_strip_pyramid_forced_overlap():
+    """The halo wait inside the strip transform (tile rows that read halo
+    rows last, producer spins on the neighbours' flags) is only enabled by
+    default when no neighbour shares the GPU; force it here so the one-GPU
+    box exercises it: the small strip tests again, with WL_STRIP_OVERLAP=2.
+    (Not the 16384^2 one: four ranks' persistent grids on ONE GPU can hold
+    every SM while waiting for a neighbour's exchange kernel that then never
+    gets scheduled -- the reason the default keeps the wait in the exchange
+    kernel when a neighbour shares the device; the 10 s timeout turns that
+    into an error, not a hang.)"""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, WL_STRIP_OVERLAP="2")
+    here = os.path.abspath(__file__)
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu",
+                        "-p", "no:cacheprovider", here, "-k",
+                        "(virtual_ranks and not large) or two_processes_ipc"],
+                       env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert " passed" in r.stdout
