@@ -2,6 +2,7 @@
 // reference's error semantics, engine dispatch, and the multi-level pyramid
 // driver (transform.cpp:198-256).
 #include <atomic>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -14,6 +15,13 @@ namespace {
 thread_local std::string g_err;
 std::atomic<long> g_launches{0};
 std::atomic<int> g_engine{0};
+// Fused level pairs in forward pyramids (wl_set_level_fusion; WL_FUSE=1
+// enables). Off by default: measured slower than one launch per level on
+// B200 except for the largest single images ("Fused levels").
+std::atomic<int> g_fuse{[] {
+    const char* v = getenv("WL_FUSE");
+    return v && v[0] == '1' ? 1 : 0;
+}()};
 
 int fail(int code, const std::string& msg) {
     g_err = msg;
@@ -109,6 +117,8 @@ const char* wl_version(void) {
 }
 
 int wl_set_engine(int engine) { return g_engine.exchange(engine); }
+
+int wl_set_level_fusion(int on) { return g_fuse.exchange(on ? 1 : 0); }
 
 long wl_launch_count(void) { return g_launches.load(); }
 
@@ -376,42 +386,26 @@ size_t wl_pyramid_elems(int w, int h, int levels) {
 
 size_t wl_pyramid_scratch_elems(int w, int h, int levels) {
     if (w <= 0 || h <= 0 || levels < 1) return 0;
-    // Two ping-pong LL buffers of the level-1 plane size.
-    return 2 * static_cast<size_t>(w / 2) * static_cast<size_t>(h / 2);
+    // Two ping-pong LL buffers of the level-1 plane size (+ the task and
+    // row counters of fused level pairs).
+    return 2 * static_cast<size_t>(w / 2) * static_cast<size_t>(h / 2) +
+           (levels > 1 ? wl_fused_ctr_elems(h / 2, 1) : 0);
 }
 
-// transform.cpp:198-227: level l transforms the previous level's LL.
+// transform.cpp:198-227: level l transforms the previous level's LL (the
+// batched path with one image: same launches, fused level pairs included).
 int wl_dwt2_pyramid_forward(const float* img, int w, int h, int levels, int wavelet, int scheme,
                             int boundary, int scaling, float* pyramid, float* scratch,
                             void* stream) {
     if (levels < 1) return fail(WL_EINVAL, "levels must be >= 1");
     if (w <= 0 || h <= 0) return fail(WL_EINVAL, "forward requires even positive dimensions");
-    const int div = 1 << levels;
+    const int div = 1 << (levels > 30 ? 30 : levels);
     if (levels > 30 || w % div != 0 || h % div != 0)
         return fail(WL_EINVAL, "image dimensions must be divisible by 2^levels");
     if (!img || !pyramid || !scratch) return fail(WL_EINVAL, "null buffer");
-    size_t off = 0;
-    const float* src = img;
-    long src_pitch = w;
-    int cw = w, ch = h;
-    float* ping[2] = {scratch, scratch + static_cast<size_t>(w / 2) * (h / 2)};
-    for (int l = 0; l < levels; ++l) {
-        const int qw = cw / 2, qh = ch / 2;
-        const size_t n = static_cast<size_t>(qw) * qh;
-        float* hl = pyramid + off;
-        float* lh = hl + n;
-        float* hh = lh + n;
-        off += 3 * n;
-        float* ll = (l + 1 == levels) ? pyramid + off : ping[l & 1];
-        const int st = wl_dwt2_forward(src, cw, ch, src_pitch, wavelet, scheme, boundary, scaling,
-                                       ll, hl, lh, hh, qw, stream);
-        if (st != WL_OK) return st;
-        src = ll;
-        src_pitch = qw;
-        cw = qw;
-        ch = qh;
-    }
-    return WL_OK;
+    const long n = static_cast<long>(w) * h;
+    return wl_dwt2_pyramid_forward_batch(img, w, h, n, 1, levels, wavelet, scheme, boundary,
+                                         scaling, pyramid, n, scratch, stream);
 }
 
 // transform.cpp:229-256: coarsest level first.
@@ -447,7 +441,10 @@ int wl_dwt2_pyramid_inverse(const float* pyramid, int w, int h, int levels, int 
 size_t wl_pyramid_batch_scratch_elems(int w, int h, int levels, int n) {
     if (w <= 0 || h <= 0 || levels < 1 || n < 1) return 0;
     const size_t q1 = static_cast<size_t>(w / 2) * (h / 2);
-    return static_cast<size_t>(n) * (q1 + (levels > 1 ? q1 / 4 : 0));
+    // LL ping-pong: n*q1 | n*(q1/4 + q1/16) (a fused pair at level 1 writes
+    // LL_1 and LL_2 side by side), then the fused-launch counters
+    return static_cast<size_t>(n) * (q1 + (levels > 1 ? q1 / 4 + q1 / 16 : 0)) +
+           (levels > 1 ? wl_fused_ctr_elems(h / 2, n) : 0);
 }
 
 // Batched multi_level_forward (transform.cpp:198-227 per image): one launch
@@ -471,25 +468,31 @@ int wl_dwt2_pyramid_forward_batch(const float* imgs, int w, int h, long img_stri
         return fail(WL_EINVAL, "batch stride too small");
     const size_t q1 = static_cast<size_t>(w / 2) * (h / 2);
     float* ping[2] = {scratch, scratch + static_cast<size_t>(n) * q1};
-    const float* src = imgs;
-    long src_stride = img_stride;
-    size_t off = 0;
-    int cw = w, ch = h;
-    for (int l = 0; l < levels; ++l) {
-        const int qw = cw / 2, qh = ch / 2;
+    unsigned* ctr = reinterpret_cast<unsigned*>(
+        scratch + static_cast<size_t>(n) * (q1 + q1 / 4 + q1 / 16));
+    size_t offs[32];  // pyramid offset of level l's HL plane
+    {
+        size_t off = 0;
+        for (int l = 0; l < levels; ++l) {
+            offs[l] = off;
+            off += 3 * static_cast<size_t>(w >> (l + 1)) * (h >> (l + 1));
+        }
+        offs[levels] = off;  // coarsest LL
+    }
+    // Level l reading `src` (batch stride src_stride), LL to `ll` (stride ll_stride).
+    auto level = [&](int l, const float* src, long src_stride, float* ll, long ll_stride) {
+        const int qw = w >> (l + 1), qh = h >> (l + 1);
         const long np = static_cast<long>(qw) * qh;
-        float* hl = pyramids + off;
-        off += 3 * np;
-        const bool last = l + 1 == levels;
+        float* hl = pyramids + offs[l];
         WlLevel L{};
         L.in[0] = src;
-        L.out[0] = last ? pyramids + off : ping[l & 1];
+        L.out[0] = ll;
         L.out[1] = hl;
         L.out[2] = hl + np;
         L.out[3] = hl + 2 * np;
         L.qw = qw;
         L.qh = qh;
-        L.in_pitch = cw;
+        L.in_pitch = 2 * qw;
         L.out_pitch = qw;
         L.wavelet = wavelet;
         L.scheme = scheme;
@@ -499,14 +502,58 @@ int wl_dwt2_pyramid_forward_batch(const float* imgs, int w, int h, long img_stri
         L.scaling = scaling != 0;
         L.nb = n;
         L.in_bstride[0] = src_stride;
-        L.out_bstride[0] = last ? pyr_stride : np;
+        L.out_bstride[0] = ll_stride;
         L.out_bstride[1] = L.out_bstride[2] = L.out_bstride[3] = pyr_stride;
-        const int st = launch_level_batch(L, static_cast<cudaStream_t>(stream));
+        return L;
+    };
+    // LL of level l: the pyramid's coarsest plane, or scratch buffer `buf` at `at`
+    auto ll_of = [&](int l, int buf, size_t at, float** p, long* stride) {
+        if (l + 1 == levels) {
+            *p = pyramids + offs[levels];
+            *stride = pyr_stride;
+        } else {
+            *p = ping[buf] + at;
+            *stride = static_cast<long>(w >> (l + 1)) * (h >> (l + 1));
+        }
+    };
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const float* src = imgs;
+    long src_stride = img_stride;
+    int inbuf = -1;  // scratch buffer holding src (-1: the images)
+    for (int l = 0; l < levels;) {
+        const int q = inbuf == 0 ? 1 : 0;  // the other buffer
+        // Two levels per launch where the fast engine can fuse them (periodic
+        // lifting forwards): LL_l is re-read from L2 by the same launch. Its
+        // level l+1 must not overwrite level l's input while tiles still read
+        // it: both LL planes go to the buffer that does not hold the input.
+        if (l + 1 < levels && g_engine.load() != 1 && g_fuse.load()) {
+            float *l0, *l1;
+            long s0, s1;
+            const size_t q_l = static_cast<size_t>(n) * (w >> (l + 1)) * (h >> (l + 1));
+            ll_of(l, q, 0, &l0, &s0);
+            if (inbuf < 0) ll_of(l + 1, 1, 0, &l1, &s1);  // level 0 fills buffer 0
+            else ll_of(l + 1, q, q_l, &l1, &s1);
+            const WlLevel L0 = level(l, src, src_stride, l0, s0);
+            const WlLevel L1 = level(l + 1, l0, s0, l1, s1);
+            const cudaError_t e = wl_launch_fast_fused(L0, L1, ctr, s);
+            if (e == cudaSuccess) {
+                src = l1;
+                src_stride = s1;
+                inbuf = inbuf < 0 ? 1 : q;
+                l += 2;
+                continue;
+            }
+            if (e != cudaErrorNotSupported) return cuda_status(e, "fast_kernel (fused levels)");
+        }
+        float* ll;
+        long ls;
+        ll_of(l, q, 0, &ll, &ls);
+        const int st = launch_level_batch(level(l, src, src_stride, ll, ls), s);
         if (st != WL_OK) return st;
-        src = L.out[0];
-        src_stride = L.out_bstride[0];
-        cw = qw;
-        ch = qh;
+        src = ll;
+        src_stride = ls;
+        inbuf = q;
+        ++l;
     }
     return WL_OK;
 }

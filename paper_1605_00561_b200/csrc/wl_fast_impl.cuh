@@ -32,6 +32,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -151,6 +152,10 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* b, unsigned parity) {
         "r"(parity), "r"(WL_PROD_HINT_NS)
         : "memory");
 }
+// Fused pyramid launches: tasks claimed per atomic.
+#ifndef WL_FUSE_CLAIM
+#define WL_FUSE_CLAIM 4
+#endif
 // Forward input tile as WL_FWD_SPLIT TMA boxes of 2*kRows/WL_FWD_SPLIT rows.
 #ifndef WL_FWD_SPLIT
 #define WL_FWD_SPLIT 1
@@ -259,6 +264,152 @@ __device__ inline void wait_halo_flags(const unsigned* fa, const unsigned* fb, u
     asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
+// Two pyramid levels in ONE persistent launch (forward, periodic): the tiles
+// of level l and of level l+1 form one task sequence over the whole batch --
+// level-l tile rows in order (global row J = b*R0 + j), each followed by the
+// level-(l+1) tile rows that become ready with it. Level-(l+1) row k of
+// image b reads LL_l rows held by level-l rows <= 2k+1+c of that image (the
+// wrapping top row k = 0 needs the image's last row and goes last); it is
+// emitted D rows later than that (D covers the tasks CTAs have claimed but
+// not finished, so its producer rarely waits). CTAs claim tasks in sequence
+// order from a global counter (ctr[0]); a level-l tile's warps count their
+// completion per tile row (ctr[1 + b*R0 + j], release); a level-(l+1) tile's
+// producer waits (acquire) for the rows of LL_l its TMA box covers.
+// Dependencies always point to earlier tasks and tasks are claimed in
+// order, so the wait cannot deadlock. LL_l is re-read while still in L2.
+struct FuseArgs {
+    unsigned* ctr;  // [0] task counter, [1 + b*R0 + j] warps done with level-l row j
+    int nb;         // images
+    int R0, R1;     // tile rows per image of level l / l+1
+    int X0n, X1n;   // tile columns
+    int c;          // level-(l+1) row k (k >= 1) needs level-l rows <= 2k+1+c
+    int D;          // emission lag in level-l rows
+    int ntasks;
+    unsigned target;  // ctr value of a finished level-l tile row (X0n * NW)
+};
+struct KArgs {
+    FastArgs lv[2];  // lv[1]: the second level of a fused launch
+    FuseArgs fu;
+};
+
+__device__ __host__ __forceinline__ int floordiv(int a, int b) {
+    return a >= 0 ? a / b : -((-a + b - 1) / b);
+}
+// Level-(l+1) rows emitted up to and including global level-l row J
+// (list order per image: k = 1..R1-1, then 0).
+__device__ __host__ __forceinline__ int fused_n1(const FuseArgs& f, int J) {
+    if (J >= f.nb * f.R0 - 1) return f.nb * f.R1;
+    if (J < 0 || f.R1 == 0) return 0;
+    // images whose rows are all emitted: J - b*R0 - D >= R0 - 1
+    int bf = floordiv(J - f.D - f.R0 + 1, f.R0) + 1;
+    bf = bf < 0 ? 0 : (bf > f.nb ? f.nb : bf);
+    int n = bf * f.R1;
+    if (bf < f.nb) {  // the one partially emitted image
+        const int jj = J - bf * f.R0 - f.D;
+        if (jj >= 0) {
+            const int v = floordiv(jj - 1 - f.c, 2);  // rows k = 1..v
+            n += v < 0 ? 0 : (v > f.R1 - 1 ? f.R1 - 1 : v);
+        }
+    }
+    return n;
+}
+// Task t -> (level, image, tile row, tile column) of a fused launch.
+__device__ __forceinline__ void fused_decode(const FuseArgs& f, int t, int& lvl, int& b, int& tyi,
+                                             int& txi, int& row_end) {
+    auto cum = [&](int J) { return (J + 1) * f.X0n + fused_n1(f, J) * f.X1n; };
+    // smallest J with cum(J) > t: estimate from the steady state (a level-l
+    // row plus half a level-(l+1) row per step, D + 1 + c rows of lag), then
+    // correct (image ends shift it by a few rows)
+    const int last = f.nb * f.R0 - 1;
+    const float x1 = f.R1 > 0 ? (float)f.X1n : 0.f;
+    int lo = (int)(((float)t + 0.5f * (float)(f.D + 1 + f.c) * x1) /
+                   ((float)f.X0n + x1 * (float)f.R1 / (float)f.R0));
+    lo = lo < 0 ? 0 : (lo > last ? last : lo);
+    while (lo > 0 && cum(lo - 1) > t) --lo;
+    while (lo < last && cum(lo) <= t) ++lo;
+    int r = t - (lo > 0 ? cum(lo - 1) : 0);
+    if (r < f.X0n) {
+        lvl = 0;
+        b = lo / f.R0;
+        tyi = lo - b * f.R0;
+        txi = r;
+        row_end = t - r + f.X0n;
+    } else {
+        r -= f.X0n;
+        const int m = r / f.X1n;
+        const int g = fused_n1(f, lo - 1) + m;  // global level-(l+1) list index
+        lvl = 1;
+        b = g / f.R1;
+        const int i = g - b * f.R1;
+        tyi = i + 1 < f.R1 ? i + 1 : 0;
+        txi = r - m * f.X1n;
+        row_end = t - txi + f.X1n;
+    }
+}
+__device__ __forceinline__ unsigned ld_acquire_gpu_u32(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned ld_relaxed_gpu_u32(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+// Producer of a level-(l+1) tile: wait until the level-l tile rows holding
+// LL_l rows [2*cy, 2*(cy + rows)) (wrapped) are complete. The (at most a
+// few) row counters are polled with independent loads -- one round trip per
+// poll -- and one acquire fence follows; `known` caches the last verified
+// row range of an image (tiles of one level-(l+1) row share it).
+struct RowCache {
+    int b = -1, lo = 0, hi = -1;
+};
+template <class Idle>
+__device__ inline void fused_wait_rows(const KArgs& K, int b, int cy, int rows, RowCache& known,
+                                       Idle&& idle) {
+    const FastArgs& a0 = K.lv[0];
+    const FuseArgs& f = K.fu;
+    const int qh0 = a0.qh;
+    const int ya = 2 * cy, yb = 2 * (cy + rows);
+    auto jof = [&](int y) { return floordiv(y - a0.Y0, a0.TH) - a0.ty0; };
+    int lo0, hi0, lo1 = 0, hi1 = -1;  // one or two row intervals
+    if (yb - ya >= qh0) {
+        lo0 = 0;
+        hi0 = f.R0 - 1;
+    } else {
+        const int y0 = ((ya % qh0) + qh0) % qh0, y1 = (((yb - 1) % qh0) + qh0) % qh0;
+        if (y0 <= y1) {
+            lo0 = jof(y0);
+            hi0 = jof(y1);
+        } else {
+            lo0 = jof(y0);
+            hi0 = f.R0 - 1;
+            hi1 = jof(y1);
+        }
+    }
+    if (hi1 < 0 && known.b == b && lo0 >= known.lo && hi0 <= known.hi) return;
+    const unsigned* c = f.ctr + 1 + (size_t)b * f.R0;
+    unsigned ns = 32;
+    for (;;) {
+        bool ok = true;
+        for (int j = lo0; j <= hi0; ++j) ok &= ld_relaxed_gpu_u32(c + j) >= f.target;
+        for (int j = lo1; j <= hi1; ++j) ok &= ld_relaxed_gpu_u32(c + j) >= f.target;
+        if (ok) break;
+        idle();  // report this CTA's own finished rows: they may be the ones missing
+        __nanosleep(ns);
+        ns = ns < 256 ? 2 * ns : 256;
+    }
+    // acquire the rows' data; LL_l was written by generic stores and the
+    // tile is read by TMA (async proxy)
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    if (hi1 < 0) {
+        known.b = b;
+        known.lo = lo0;
+        known.hi = hi0;
+    }
+}
+
 template <int R, int NW, int CPT, int NS = 2, int NXC = 4>
 struct Geometry {
     static constexpr int kStages = NS;                       // TMA ring depth
@@ -348,12 +499,20 @@ constexpr int xch_comps() {
     return mx;
 }
 
-template <class P, int DIR, int R, int NW, int CPT, int NS, bool XF, bool MIRROR>
+template <class P, int DIR, int R, int NW, int CPT, int NS, bool XF, bool MIRROR,
+          bool FUSED = false>
 __global__ void __launch_bounds__((NW + 1) * 32,
                                   (Geometry<R, NW, CPT, NS, xch_comps<P, XF>()>::kMinBlocks))
     fast_kernel(const __grid_constant__ CUtensorMap m0, const __grid_constant__ CUtensorMap m1,
                 const __grid_constant__ CUtensorMap m2, const __grid_constant__ CUtensorMap m3,
-                const FastArgs a) {
+                const __grid_constant__ KArgs K) {
+    static_assert(!FUSED || (DIR == 0 && !MIRROR), "fused launches: periodic forwards");
+    __shared__ int4 task_sm[NS];  // fused: the task of each stage (producer -> consumers)
+    // fused: per processed tile (ring of kRing), warps done storing / its level-l row
+    constexpr int kRing = 8;
+    static_assert(kRing > NS, "report ring");
+    __shared__ unsigned done_cnt[kRing];
+    __shared__ int row_ring[kRing];
     constexpr int NXC = xch_comps<P, XF>();
     using G = Geometry<R, NW, CPT, NS, NXC>;
     constexpr int H = P::kHalo;
@@ -365,12 +524,15 @@ __global__ void __launch_bounds__((NW + 1) * 32,
     uint64_t* full = reinterpret_cast<uint64_t*>(xch + G::kXchFloats);
     uint64_t* empty = full + NS;
 
+    const FastArgs& a = K.lv[0];  // per-tile code rebinds it to the tile's level
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
         for (int k = 0; k < NS; ++k) {
             mbar_init(&full[k], 1);
             mbar_init(&empty[k], NW * 32);
         }
+        if (FUSED)
+            for (int k = 0; k < kRing; ++k) done_cnt[k] = 0;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -381,7 +543,113 @@ __global__ void __launch_bounds__((NW + 1) * 32,
 
     if (warp == NW) {
         // ---------------- producer warp: TMA tile stream ----------------
-        if (lane == 0) {
+        if (FUSED && lane == 0) {
+            // Tasks are claimed in chunks of kClaim, the next chunk one chunk
+            // ahead, so the claim's round trip never stalls the TMA stream.
+            constexpr int kClaim = WL_FUSE_CLAIM;
+#ifdef WL_FUSE_STATIC  // diagnostic: static round-robin chunks (no dependency-safe order!)
+            int base = blockIdx.x * kClaim, k_in = 0;
+            int next = base + gridDim.x * kClaim;
+#else
+            int base = atomicAdd(K.fu.ctr, kClaim), k_in = 0;
+            int next = atomicAdd(K.fu.ctr, kClaim);
+#endif
+            RowCache known;
+            int lvl = 0, b = 0, tyi = 0, txi = 0, row_end = -1, prev = -2;
+            // Completion reports of level-l tile rows: the compute warps count
+            // their finished stores per tile in shared memory (release.cta);
+            // this thread turns them, in order, into per-row global counts
+            // (one GPU-scope fence per run of tiles of one row) -- the fence's
+            // wait for outstanding stores is taken here, not by compute warps.
+            int sig = 0, prow = -1;
+            unsigned pcnt = 0;
+            auto flush = [&]() {
+                if (prow >= 0) {
+                    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                    asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(
+                                     K.fu.ctr + 1 + prow), "r"(pcnt) : "memory");
+                    prow = -1;
+                    pcnt = 0;
+                }
+            };
+            auto report = [&](int upto, bool wait) {  // tiles [sig, upto)
+                while (sig < upto) {
+                    const int sl = sig & (kRing - 1);
+                    unsigned c;
+                    asm volatile("ld.acquire.cta.shared.u32 %0, [%1];"
+                                 : "=r"(c) : "r"(smem_u32(&done_cnt[sl])) : "memory");
+                    if (c < NW) {
+                        if (!wait) return;
+                        __nanosleep(32);
+                        continue;
+                    }
+                    done_cnt[sl] = 0;
+                    const int row = row_ring[sl];
+                    if (row >= 0) {
+                        if (row != prow) flush();
+                        prow = row;
+                        pcnt += NW;
+                    }
+                    ++sig;
+                }
+            };
+            int issued = 0;
+            auto idle = [&]() {
+                report(issued, false);
+                flush();
+            };
+            auto wait_empty = [&](int s_, unsigned ph) {
+                unsigned ns = 32;
+                for (int polls = 0; !mbar_test(&empty[s_], ph); ++polls) {
+                    report(issued, false);
+                    if (polls > 4) flush();
+                    __nanosleep(ns);
+                    ns = ns < WL_PROD_BACKOFF_NS ? 2 * ns : WL_PROD_BACKOFF_NS;
+                }
+            };
+            for (int i = 0;; ++i) {
+                const int t = base + k_in;
+                const int s = i % NS;
+                const unsigned use = i / NS;
+                if (t >= K.fu.ntasks) {
+                    if (i >= NS) wait_empty(s, (use - 1) & 1);
+                    task_sm[s] = make_int4(-1, 0, 0, 0);
+                    mbar_arrive(&full[s]);  // consumers see the sentinel and stop
+                    report(issued, true);
+                    flush();
+                    break;
+                }
+                // consecutive task in the same tile row: next column
+                if (t == prev + 1 && t < row_end) ++txi;
+                else fused_decode(K.fu, t, lvl, b, tyi, txi, row_end);
+                prev = t;
+                const FastArgs& a = K.lv[lvl];
+                const int cx = a.X0 + (txi + a.tx0) * a.TW - HX;
+                const int cy = a.Y0 + (tyi + a.ty0) * a.TH - H - 1;
+                if (lvl == 1) fused_wait_rows(K, b, cy, G::kRows, known, idle);
+                if (i >= NS) wait_empty(s, (use - 1) & 1);
+                report(i - kRing + 1, true);  // ring slot i % kRing is free
+                row_ring[i & (kRing - 1)] = lvl == 0 ? b * K.fu.R0 + tyi : -1;
+                issued = i + 1;
+                task_sm[s] = make_int4(lvl, b, tyi, txi);
+                float* dst = stage + s * G::kStageFloats;
+                mbar_expect_tx(&full[s], G::kStageBytes);
+                constexpr int kSplitRows = 2 * G::kRows / WL_FWD_SPLIT;
+#pragma unroll
+                for (int q = 0; q < WL_FWD_SPLIT; ++q)
+                    tma_load_3d(dst + q * kSplitRows * 2 * TWC, lvl ? &m1 : &m0, &full[s], 2 * cx,
+                                2 * cy + q * kSplitRows, b);
+                if (++k_in == kClaim) {
+                    base = next;
+                    k_in = 0;
+#ifdef WL_FUSE_STATIC
+                    next = base + gridDim.x * kClaim;
+#else
+                    if (base < K.fu.ntasks) next = atomicAdd(K.fu.ctr, kClaim);
+#endif
+                }
+            }
+        } else if (lane == 0) {
             bool halo_ready = false;
             for (int i = 0, t = blockIdx.x; t < a.ntiles; t += gridDim.x) {
                 if (a.filter) {  // interior-only / border-only launch of a symmetric plan
@@ -436,422 +704,458 @@ __global__ void __launch_bounds__((NW + 1) * 32,
     }
 
     // ---------------- compute warps ----------------
+    // Fused launches: a warp reports a level-l tile row done (ctr += 1,
+    // release) one tile later, right before its next stores, when its
+    // previous stores have long drained -- the fence then costs nothing.
     float v[R][CPT][4];
     float gu[CPT][4], gd[CPT][4];
     int xslot = 0;
 
-    for (int i = 0, t = blockIdx.x; t < a.ntiles; t += gridDim.x) {
+    for (int i = 0, t = blockIdx.x;; t += gridDim.x) {
         const int s = i % NS;
-        const int b = t / a.ntiles_img, tt = t - b * a.ntiles_img;
-        const int tyk = tt / a.tiles_x;
-        const int tyi = tile_row_of(tyk, a.ntiles_img / a.tiles_x, a.xflag_a != nullptr);
-        const int ty = tyi + a.ty0, tx = tt - tyk * a.tiles_x + a.tx0;
-        const int cx = a.X0 + tx * a.TW - HX;     // first compute cell column
-        const int cy = a.Y0 + ty * a.TH - H - 1;  // ghost row above the region
-        // Border tile: its compute region leaves the image. Periodic plans
-        // load its cells with wrapped coordinates straight from global memory
-        // (load-time wrap is exact for the periodic extension).
-        const bool border = cx < 0 || cy < 0 || cx + TWC > a.qw || cy + G::kRows > a.qh;
-        if (a.filter && border != (a.filter == 2)) continue;  // the other launch's tile
-        const unsigned phase = (i / NS) & 1;  // fill count of stage s (processed tiles)
-        ++i;
-        const bool wrap_tile = a.wrap && border;
-        // Symmetric border tile: out-of-image cells come zero-filled from the
-        // TMA box and are never read as such -- before every neighbour step
-        // the distance-1 ghosts are overwritten with their mirror images.
-        const bool mtile = MIRROR && a.mirror && border;
-        const int gy0m = cy + 1 + warp * R;  // image row of v[0]
-        mbar_wait(&full[s], phase);
-        const float* st = stage + s * G::kStageFloats;
+        int b, tyi, txi, lvl = 0;
+        if constexpr (FUSED) {
+            mbar_wait(&full[s], (i / NS) & 1);
+            const int4 tk = task_sm[s];
+            if (tk.x < 0) break;
+            lvl = tk.x;
+            b = tk.y;
+            tyi = tk.z;
+            txi = tk.w;
+        } else {
+            const FastArgs& a0 = K.lv[0];
+            if (t >= a0.ntiles) break;
+            b = t / a0.ntiles_img;
+            const int tt = t - b * a0.ntiles_img;
+            const int tyk = tt / a0.tiles_x;
+            tyi = tile_row_of(tyk, a0.ntiles_img / a0.tiles_x, a0.xflag_a != nullptr);
+            txi = tt - tyk * a0.tiles_x;
+        }
+        // The tile body, instantiated per level with compile-time offsets into
+        // K.lv[] (a register-indexed parameter load stalls like a memory load).
+        auto body = [&](auto L_) {
+            const FastArgs& a = K.lv[decltype(L_)::value];
+            const int ty = tyi + a.ty0, tx = txi + a.tx0;
+            const int cx = a.X0 + tx * a.TW - HX;     // first compute cell column
+            const int cy = a.Y0 + ty * a.TH - H - 1;  // ghost row above the region
+            // Border tile: its compute region leaves the image. Periodic plans
+            // load its cells with wrapped coordinates straight from global memory
+            // (load-time wrap is exact for the periodic extension).
+            const bool border = cx < 0 || cy < 0 || cx + TWC > a.qw || cy + G::kRows > a.qh;
+            if (a.filter && border != (a.filter == 2)) return;  // the other launch's tile
+            const unsigned phase = (i / NS) & 1;  // fill count of stage s (processed tiles)
+            ++i;
+            const bool wrap_tile = a.wrap && border;
+            // Symmetric border tile: out-of-image cells come zero-filled from the
+            // TMA box and are never read as such -- before every neighbour step
+            // the distance-1 ghosts are overwritten with their mirror images.
+            const bool mtile = MIRROR && a.mirror && border;
+            const int gy0m = cy + 1 + warp * R;  // image row of v[0]
+            if constexpr (!FUSED) mbar_wait(&full[s], phase);
+            const float* st = stage + s * G::kStageFloats;
 
-        // Load the warp's rows (+ one ghost row above and below) and split
-        // the 2x2 polyphase components.
-        auto load_row = [&](int q, float (&dst)[CPT][4]) {
-            // q: cell row in the stage (0 = ghost row above the region)
-            if (wrap_tile) {
-                // periodic wrap: one conditional add/subtract unless the image
-                // is smaller than a tile (then the general modulo)
-                const bool small = WL_WRAP_MOD_INV && DIR == 1 || a.qw < TWC || a.qh < G::kRows;
-                auto wrapi = [small](int i, int n) {
-                    if (small) {
-                        i %= n;
-                        return i < 0 ? i + n : i;
+            // Load the warp's rows (+ one ghost row above and below) and split
+            // the 2x2 polyphase components.
+            auto load_row = [&](int q, float (&dst)[CPT][4]) {
+                // q: cell row in the stage (0 = ghost row above the region)
+                if (wrap_tile) {
+                    // periodic wrap: one conditional add/subtract unless the image
+                    // is smaller than a tile (then the general modulo)
+                    const bool small = WL_WRAP_MOD_INV && DIR == 1 || a.qw < TWC || a.qh < G::kRows;
+                    auto wrapi = [small](int i, int n) {
+                        if (small) {
+                            i %= n;
+                            return i < 0 ? i + n : i;
+                        }
+                        return i < 0 ? i + n : (i >= n ? i - n : i);
+                    };
+                    const int ry = wrapi(cy + q, a.qh);
+#pragma unroll
+                    for (int j = 0; j < CPT; ++j) {
+                        const int rx = wrapi(cx + CPT * lane + j, a.qw);
+                        if (DIR == 0) {
+                            const float* p =
+                                a.in[0] + b * a.in_bstride[0] + (long)(2 * ry) * a.in_pitch + 2 * rx;
+                            const float2 u0 = *reinterpret_cast<const float2*>(p);
+                            const float2 u1 = *reinterpret_cast<const float2*>(p + a.in_pitch);
+                            dst[j][0] = u0.x;
+                            dst[j][1] = u0.y;
+                            dst[j][2] = u1.x;
+                            dst[j][3] = u1.y;
+                        } else {
+#pragma unroll
+                            for (int c = 0; c < 4; ++c)
+                                dst[j][c] = a.in[c][b * a.in_bstride[c] + (long)ry * a.in_pitch + rx];
+                        }
                     }
-                    return i < 0 ? i + n : (i >= n ? i - n : i);
-                };
-                const int ry = wrapi(cy + q, a.qh);
-#pragma unroll
-                for (int j = 0; j < CPT; ++j) {
-                    const int rx = wrapi(cx + CPT * lane + j, a.qw);
-                    if (DIR == 0) {
-                        const float* p =
-                            a.in[0] + b * a.in_bstride[0] + (long)(2 * ry) * a.in_pitch + 2 * rx;
-                        const float2 u0 = *reinterpret_cast<const float2*>(p);
-                        const float2 u1 = *reinterpret_cast<const float2*>(p + a.in_pitch);
-                        dst[j][0] = u0.x;
-                        dst[j][1] = u0.y;
-                        dst[j][2] = u1.x;
-                        dst[j][3] = u1.y;
-                    } else {
-#pragma unroll
-                        for (int c = 0; c < 4; ++c)
-                            dst[j][c] = a.in[c][b * a.in_bstride[c] + (long)ry * a.in_pitch + rx];
-                    }
-                }
-            } else if (DIR == 0) {
-                // pixel rows 2q (LL HL LL HL ...) and 2q+1 (LH HH ...)
-                const float* p0 = st + (2 * q) * (2 * TWC) + 2 * CPT * lane;
-                float4 e[CPT / 2], o[CPT / 2];
-                if constexpr (CPT == 4) {
-                    // lanes 32 B apart: read the two 16-B halves in an order
-                    // swizzled by lane group so every 8-lane phase covers all
-                    // 32 banks (no 2-way conflict), then undo the swap
-#if WL_LDS_SWIZZLE
-                    const int sw = (lane >> 2) & 1;
-                    const float4 e0 = *reinterpret_cast<const float4*>(p0 + 4 * sw);
-                    const float4 e1 = *reinterpret_cast<const float4*>(p0 + 4 * (sw ^ 1));
-                    const float4 o0 = *reinterpret_cast<const float4*>(p0 + 2 * TWC + 4 * sw);
-                    const float4 o1 = *reinterpret_cast<const float4*>(p0 + 2 * TWC + 4 * (sw ^ 1));
-                    e[0] = sw ? e1 : e0;
-                    e[1] = sw ? e0 : e1;
-                    o[0] = sw ? o1 : o0;
-                    o[1] = sw ? o0 : o1;
-#else
-                    e[0] = *reinterpret_cast<const float4*>(p0);
-                    e[1] = *reinterpret_cast<const float4*>(p0 + 4);
-                    o[0] = *reinterpret_cast<const float4*>(p0 + 2 * TWC);
-                    o[1] = *reinterpret_cast<const float4*>(p0 + 2 * TWC + 4);
-#endif
-                } else {
-                    e[0] = *reinterpret_cast<const float4*>(p0);
-                    o[0] = *reinterpret_cast<const float4*>(p0 + 2 * TWC);
-                }
-#pragma unroll
-                for (int jj = 0; jj < CPT / 2; ++jj) {
-                    dst[2 * jj][0] = e[jj].x; dst[2 * jj][1] = e[jj].y;
-                    dst[2 * jj][2] = o[jj].x; dst[2 * jj][3] = o[jj].y;
-                    dst[2 * jj + 1][0] = e[jj].z; dst[2 * jj + 1][1] = e[jj].w;
-                    dst[2 * jj + 1][2] = o[jj].z; dst[2 * jj + 1][3] = o[jj].w;
-                }
-            } else {
-                constexpr int plane = TWC * G::kRows;
-#pragma unroll
-                for (int c = 0; c < 4; ++c) {
-                    const float* p = st + c * plane + q * TWC + CPT * lane;
+                } else if (DIR == 0) {
+                    // pixel rows 2q (LL HL LL HL ...) and 2q+1 (LH HH ...)
+                    const float* p0 = st + (2 * q) * (2 * TWC) + 2 * CPT * lane;
+                    float4 e[CPT / 2], o[CPT / 2];
                     if constexpr (CPT == 4) {
-                        const float4 u = *reinterpret_cast<const float4*>(p);
-                        dst[0][c] = u.x; dst[1][c] = u.y; dst[2][c] = u.z; dst[3][c] = u.w;
+                        // lanes 32 B apart: read the two 16-B halves in an order
+                        // swizzled by lane group so every 8-lane phase covers all
+                        // 32 banks (no 2-way conflict), then undo the swap
+#if WL_LDS_SWIZZLE
+                        const int sw = (lane >> 2) & 1;
+                        const float4 e0 = *reinterpret_cast<const float4*>(p0 + 4 * sw);
+                        const float4 e1 = *reinterpret_cast<const float4*>(p0 + 4 * (sw ^ 1));
+                        const float4 o0 = *reinterpret_cast<const float4*>(p0 + 2 * TWC + 4 * sw);
+                        const float4 o1 = *reinterpret_cast<const float4*>(p0 + 2 * TWC + 4 * (sw ^ 1));
+                        e[0] = sw ? e1 : e0;
+                        e[1] = sw ? e0 : e1;
+                        o[0] = sw ? o1 : o0;
+                        o[1] = sw ? o0 : o1;
+#else
+                        e[0] = *reinterpret_cast<const float4*>(p0);
+                        e[1] = *reinterpret_cast<const float4*>(p0 + 4);
+                        o[0] = *reinterpret_cast<const float4*>(p0 + 2 * TWC);
+                        o[1] = *reinterpret_cast<const float4*>(p0 + 2 * TWC + 4);
+#endif
                     } else {
-                        const float2 u = *reinterpret_cast<const float2*>(p);
-                        dst[0][c] = u.x;
-                        dst[1][c] = u.y;
+                        e[0] = *reinterpret_cast<const float4*>(p0);
+                        o[0] = *reinterpret_cast<const float4*>(p0 + 2 * TWC);
                     }
+#pragma unroll
+                    for (int jj = 0; jj < CPT / 2; ++jj) {
+                        dst[2 * jj][0] = e[jj].x; dst[2 * jj][1] = e[jj].y;
+                        dst[2 * jj][2] = o[jj].x; dst[2 * jj][3] = o[jj].y;
+                        dst[2 * jj + 1][0] = e[jj].z; dst[2 * jj + 1][1] = e[jj].w;
+                        dst[2 * jj + 1][2] = o[jj].z; dst[2 * jj + 1][3] = o[jj].w;
+                    }
+                } else {
+                    constexpr int plane = TWC * G::kRows;
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        const float* p = st + c * plane + q * TWC + CPT * lane;
+                        if constexpr (CPT == 4) {
+                            const float4 u = *reinterpret_cast<const float4*>(p);
+                            dst[0][c] = u.x; dst[1][c] = u.y; dst[2][c] = u.z; dst[3][c] = u.w;
+                        } else {
+                            const float2 u = *reinterpret_cast<const float2*>(p);
+                            dst[0][c] = u.x;
+                            dst[1][c] = u.y;
+                        }
+                    }
+                }
+            };
+            load_row(warp * R, gu);
+#pragma unroll
+            for (int r = 0; r < R; ++r) load_row(warp * R + 1 + r, v[r]);
+            load_row(warp * R + R + 1, gd);
+            // Release the stage: every lane's own loads are ordered before its
+            // arrive (release semantics; a single elected arrive after __syncwarp
+            // let the next TMA overwrite rows other lanes had not finished
+            // reading), and the proxy fence orders these generic-proxy reads
+            // before the async-proxy (TMA) writes of the refill.
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_arrive(&empty[s]);
+
+            if (DIR == 1 && a.scaling) {  // undo scaling first (transform.cpp:180)
+#pragma unroll
+                for (int c = 0; c < CPT; ++c) {
+                    gu[c][0] *= a.scale; gu[c][3] /= a.scale;
+                    gd[c][0] *= a.scale; gd[c][3] /= a.scale;
+#pragma unroll
+                    for (int r = 0; r < R; ++r) { v[r][c][0] *= a.scale; v[r][c][3] /= a.scale; }
                 }
             }
-        };
-        load_row(warp * R, gu);
-#pragma unroll
-        for (int r = 0; r < R; ++r) load_row(warp * R + 1 + r, v[r]);
-        load_row(warp * R + R + 1, gd);
-        // Release the stage: every lane's own loads are ordered before its
-        // arrive (release semantics; a single elected arrive after __syncwarp
-        // let the next TMA overwrite rows other lanes had not finished
-        // reading), and the proxy fence orders these generic-proxy reads
-        // before the async-proxy (TMA) writes of the refill.
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_arrive(&empty[s]);
-
-        if (DIR == 1 && a.scaling) {  // undo scaling first (transform.cpp:180)
 #pragma unroll
             for (int c = 0; c < CPT; ++c) {
-                gu[c][0] *= a.scale; gu[c][3] /= a.scale;
-                gd[c][0] *= a.scale; gd[c][3] /= a.scale;
+                P::pre(gu[c]);
+                P::pre(gd[c]);
 #pragma unroll
-                for (int r = 0; r < R; ++r) { v[r][c][0] *= a.scale; v[r][c][3] /= a.scale; }
+                for (int r = 0; r < R; ++r) P::pre(v[r][c]);
             }
-        }
-#pragma unroll
-        for (int c = 0; c < CPT; ++c) {
-            P::pre(gu[c]);
-            P::pre(gd[c]);
-#pragma unroll
-            for (int r = 0; r < R; ++r) P::pre(v[r][c]);
-        }
 
 #ifndef WL_DIAG_NO_COMPUTE
-        sfor<P::kEpochs>([&](auto e_) {
-            constexpr int E = decltype(e_)::value;
-            constexpr unsigned long long U = P::kUse[E];
-            // Split-phase block barrier for epochs > 0: publish the edge rows
-            // and ARRIVE, compute the rows that need no neighbour-warp data,
-            // then WAIT and finish the two edge rows. Still exactly one
-            // barrier (one mbarrier phase) per epoch per tile.
-            // Layout [slot][warp][top|bottom][column c][lane] float4: every
-            // warp-wide access is a contiguous 512 B run (4 wavefronts).
-            // Published component rows of this epoch: the warp's bottom row for
-            // the components the warp below reads from its row above (UP), then
-            // its top row for those the warp above reads from below (DN). Each
-            // row is [lane] x CPT floats: one contiguous warp-wide access.
-            constexpr int NUP = xch_count(U, -1, XF), NDN = xch_count(U, 1, XF);
-            constexpr int kCompF = 32 * CPT;
-            constexpr int kSlotF = NXC * kCompF;
-            float* xw = xch + (xslot * NW + warp) * kSlotF;
-            auto put = [&](float* dst, const float (&row)[CPT][4], int C) {
-                if constexpr (CPT == 4)
-                    reinterpret_cast<float4*>(dst)[lane] =
-                        make_float4(row[0][C], row[1][C], row[2][C], row[3][C]);
-                else
-                    reinterpret_cast<float2*>(dst)[lane] = make_float2(row[0][C], row[1][C]);
-            };
-            auto get = [&](const float* src, float (&row)[CPT][4], int C) {
-                if constexpr (CPT == 4) {
-                    const float4 q = reinterpret_cast<const float4*>(src)[lane];
-                    row[0][C] = q.x; row[1][C] = q.y; row[2][C] = q.z; row[3][C] = q.w;
-                } else {
-                    const float2 q = reinterpret_cast<const float2*>(src)[lane];
-                    row[0][C] = q.x; row[1][C] = q.y;
-                }
-            };
-            if constexpr (E > 0) {
-                sfor<4>([&](auto c_) {
-                    constexpr int C = decltype(c_)::value;
-                    if constexpr (xch_up(U, C, XF))
-                        put(xw + xch_rank(U, C, -1, XF) * kCompF, v[R - 1], C);
-                    if constexpr (xch_dn(U, C, XF))
-                        put(xw + (NUP + xch_rank(U, C, 1, XF)) * kCompF, v[0], C);
-                });
-#ifdef WL_BREAK_BARRIER
-                // negative control (acceptance.cpp:283-296 / parsim break_barrier):
-                // drop the barrier of epoch WL_BREAK_BARRIER; racecheck must flag it
-                if constexpr (E != WL_BREAK_BARRIER)
-#endif
-                named_sync(1, NW * 32);  // the epoch's block barrier
-            }
-            // Symmetric border tiles (MIRROR kernel): whole-point mirroring on
-            // the component grid, per step (transform.cpp:66-71, 114-115).
-            // Every step reads at most one cell away, so before the step the
-            // distance-1 ghosts that in-image cells read are overwritten with
-            // their mirror images: row -1 := row 1, row qh := row qh-2,
-            // column -1 := column 1, column qw := column qw-2 (corners via
-            // both). The host picks the grid's row offset so that the source
-            // rows always lie in the warp's own registers (plan_tiles).
-            // vrow(T): block row T in [-1, R] (gu, v[0..R-1], gd).
-            auto vfix = [&](auto gdgu) {  // gdgu: false -> targets in v, true -> gu/gd
-                if (!mtile) return;
-                const int t_top = -gy0m - 1;  // block row holding image row -1
-                const int t_bot = a.qh - gy0m;  // block row holding image row qh
-                sfor<R + 2>([&](auto k_) {
-                    constexpr int T = decltype(k_)::value - 1;
-                    constexpr bool edge = T < 0 || T >= R;
-                    if constexpr (edge == decltype(gdgu)::value) {
-                        float (&dst)[CPT][4] = T < 0 ? gu : (T >= R ? gd : v[T < 0 ? 0 : (T >= R ? R - 1 : T)]);
-                        if constexpr (T + 2 <= R - 1) {
-                            if (T == t_top)
-                                sfor<4>([&](auto c_) {
-                                    constexpr int C = decltype(c_)::value;
-                                    if constexpr (uses_dr(U, C, -1))
-#pragma unroll
-                                        for (int c = 0; c < CPT; ++c) dst[c][C] = v[T + 2][c][C];
-                                });
-                        }
-                        if constexpr (T - 2 >= 0) {
-                            if (T == t_bot)
-                                sfor<4>([&](auto c_) {
-                                    constexpr int C = decltype(c_)::value;
-                                    if constexpr (uses_dr(U, C, 1))
-#pragma unroll
-                                        for (int c = 0; c < CPT; ++c) dst[c][C] = v[T - 2][c][C];
-                                });
-                        }
+            sfor<P::kEpochs>([&](auto e_) {
+                constexpr int E = decltype(e_)::value;
+                constexpr unsigned long long U = P::kUse[E];
+                // Split-phase block barrier for epochs > 0: publish the edge rows
+                // and ARRIVE, compute the rows that need no neighbour-warp data,
+                // then WAIT and finish the two edge rows. Still exactly one
+                // barrier (one mbarrier phase) per epoch per tile.
+                // Layout [slot][warp][top|bottom][column c][lane] float4: every
+                // warp-wide access is a contiguous 512 B run (4 wavefronts).
+                // Published component rows of this epoch: the warp's bottom row for
+                // the components the warp below reads from its row above (UP), then
+                // its top row for those the warp above reads from below (DN). Each
+                // row is [lane] x CPT floats: one contiguous warp-wide access.
+                constexpr int NUP = xch_count(U, -1, XF), NDN = xch_count(U, 1, XF);
+                constexpr int kCompF = 32 * CPT;
+                constexpr int kSlotF = NXC * kCompF;
+                float* xw = xch + (xslot * NW + warp) * kSlotF;
+                auto put = [&](float* dst, const float (&row)[CPT][4], int C) {
+                    if constexpr (CPT == 4)
+                        reinterpret_cast<float4*>(dst)[lane] =
+                            make_float4(row[0][C], row[1][C], row[2][C], row[3][C]);
+                    else
+                        reinterpret_cast<float2*>(dst)[lane] = make_float2(row[0][C], row[1][C]);
+                };
+                auto get = [&](const float* src, float (&row)[CPT][4], int C) {
+                    if constexpr (CPT == 4) {
+                        const float4 q = reinterpret_cast<const float4*>(src)[lane];
+                        row[0][C] = q.x; row[1][C] = q.y; row[2][C] = q.z; row[3][C] = q.w;
+                    } else {
+                        const float2 q = reinterpret_cast<const float2*>(src)[lane];
+                        row[0][C] = q.x; row[1][C] = q.y;
                     }
-                });
-            };
-            // horizontal: the lane whose first cell is column 0 reads its left
-            // neighbour as its own column 1; the lane whose last cell is column
-            // qw-1 reads its right neighbour as its own column qw-2 (cx and qw
-            // are multiples of CPT).
-            auto hfix = [&](float (&sl_)[R + 2][4], float (&sr_)[R + 2][4], int r_lo, int r_hi) {
-                if (!mtile) return;
-                const int gxl = cx + CPT * lane;
-                const bool left = gxl == 0, right = gxl + CPT - 1 == a.qw - 1;
-#pragma unroll
-                for (int r = 0; r < R + 2; ++r) {
-                    if (r < r_lo || r > r_hi) continue;
-                    const float (&src)[CPT][4] =
-                        r == 0 ? gu : (r == R + 1 ? gd : v[r == 0 ? 0 : (r > R ? R - 1 : r - 1)]);
+                };
+                if constexpr (E > 0) {
                     sfor<4>([&](auto c_) {
                         constexpr int C = decltype(c_)::value;
-                        if constexpr (uses_dc(U, C, -1))
-                            if (left) sl_[r][C] = src[1][C];
-                        if constexpr (uses_dc(U, C, 1))
-                            if (right) sr_[r][C] = src[CPT - 2][C];
+                        if constexpr (xch_up(U, C, XF))
+                            put(xw + xch_rank(U, C, -1, XF) * kCompF, v[R - 1], C);
+                        if constexpr (xch_dn(U, C, XF))
+                            put(xw + (NUP + xch_rank(U, C, 1, XF)) * kCompF, v[0], C);
                     });
+#ifdef WL_BREAK_BARRIER
+                    // negative control (acceptance.cpp:283-296 / parsim break_barrier):
+                    // drop the barrier of epoch WL_BREAK_BARRIER; racecheck must flag it
+                    if constexpr (E != WL_BREAK_BARRIER)
+#endif
+                    named_sync(1, NW * 32);  // the epoch's block barrier
                 }
-            };
-            if constexpr (MIRROR) vfix(std::false_type{});
-            // Horizontal neighbours of the lane's edge columns (warp shuffle).
-            float sl[R + 2][4], sr[R + 2][4];
-            sfor<4>([&](auto c_) {
-                constexpr int C = decltype(c_)::value;
-                if constexpr (uses_dc(U, C, -1)) {
+                // Symmetric border tiles (MIRROR kernel): whole-point mirroring on
+                // the component grid, per step (transform.cpp:66-71, 114-115).
+                // Every step reads at most one cell away, so before the step the
+                // distance-1 ghosts that in-image cells read are overwritten with
+                // their mirror images: row -1 := row 1, row qh := row qh-2,
+                // column -1 := column 1, column qw := column qw-2 (corners via
+                // both). The host picks the grid's row offset so that the source
+                // rows always lie in the warp's own registers (plan_tiles).
+                // vrow(T): block row T in [-1, R] (gu, v[0..R-1], gd).
+                auto vfix = [&](auto gdgu) {  // gdgu: false -> targets in v, true -> gu/gd
+                    if (!mtile) return;
+                    const int t_top = -gy0m - 1;  // block row holding image row -1
+                    const int t_bot = a.qh - gy0m;  // block row holding image row qh
+                    sfor<R + 2>([&](auto k_) {
+                        constexpr int T = decltype(k_)::value - 1;
+                        constexpr bool edge = T < 0 || T >= R;
+                        if constexpr (edge == decltype(gdgu)::value) {
+                            float (&dst)[CPT][4] = T < 0 ? gu : (T >= R ? gd : v[T < 0 ? 0 : (T >= R ? R - 1 : T)]);
+                            if constexpr (T + 2 <= R - 1) {
+                                if (T == t_top)
+                                    sfor<4>([&](auto c_) {
+                                        constexpr int C = decltype(c_)::value;
+                                        if constexpr (uses_dr(U, C, -1))
 #pragma unroll
-                    for (int r = 0; r < R; ++r)
-                        sl[r + 1][C] = __shfl_up_sync(0xffffffffu, v[r][CPT - 1][C], 1);
-                }
-                if constexpr (uses_dc(U, C, 1)) {
+                                            for (int c = 0; c < CPT; ++c) dst[c][C] = v[T + 2][c][C];
+                                    });
+                            }
+                            if constexpr (T - 2 >= 0) {
+                                if (T == t_bot)
+                                    sfor<4>([&](auto c_) {
+                                        constexpr int C = decltype(c_)::value;
+                                        if constexpr (uses_dr(U, C, 1))
 #pragma unroll
-                    for (int r = 0; r < R; ++r)
-                        sr[r + 1][C] = __shfl_down_sync(0xffffffffu, v[r][0][C], 1);
-                }
-            });
-            if constexpr (MIRROR) hfix(sl, sr, 1, R);
-            float o[R][CPT][4];
-            auto row = [&](auto r_) {
-                sfor<CPT>([&](auto c_) {
-                    constexpr int RR = decltype(r_)::value, CC = decltype(c_)::value;
-                    Acc<R, CPT, RR, CC> acc{v, gu, gd, sl, sr};
-                    P::template nbr<E>(acc, o[RR][CC]);
-                });
-            };
-            // interior rows 1..R-2 read only this warp's rows
-            sfor<R - 2>([&](auto r_) { row(std::integral_constant<int, decltype(r_)::value + 1>{}); });
-            if constexpr (E > 0) {
+                                            for (int c = 0; c < CPT; ++c) dst[c][C] = v[T - 2][c][C];
+                                    });
+                            }
+                        }
+                    });
+                };
+                // horizontal: the lane whose first cell is column 0 reads its left
+                // neighbour as its own column 1; the lane whose last cell is column
+                // qw-1 reads its right neighbour as its own column qw-2 (cx and qw
+                // are multiples of CPT).
+                auto hfix = [&](float (&sl_)[R + 2][4], float (&sr_)[R + 2][4], int r_lo, int r_hi) {
+                    if (!mtile) return;
+                    const int gxl = cx + CPT * lane;
+                    const bool left = gxl == 0, right = gxl + CPT - 1 == a.qw - 1;
+#pragma unroll
+                    for (int r = 0; r < R + 2; ++r) {
+                        if (r < r_lo || r > r_hi) continue;
+                        const float (&src)[CPT][4] =
+                            r == 0 ? gu : (r == R + 1 ? gd : v[r == 0 ? 0 : (r > R ? R - 1 : r - 1)]);
+                        sfor<4>([&](auto c_) {
+                            constexpr int C = decltype(c_)::value;
+                            if constexpr (uses_dc(U, C, -1))
+                                if (left) sl_[r][C] = src[1][C];
+                            if constexpr (uses_dc(U, C, 1))
+                                if (right) sr_[r][C] = src[CPT - 2][C];
+                        });
+                    }
+                };
+                if constexpr (MIRROR) vfix(std::false_type{});
+                // Horizontal neighbours of the lane's edge columns (warp shuffle).
+                float sl[R + 2][4], sr[R + 2][4];
                 sfor<4>([&](auto c_) {
                     constexpr int C = decltype(c_)::value;
-                    if constexpr (xch_up(U, C, XF))  // bottom row of the warp above
-                        if (warp > 0) get(xw - kSlotF + xch_rank(U, C, -1, XF) * kCompF, gu, C);
-                    if constexpr (xch_dn(U, C, XF))  // top row of the warp below
-                        if (warp < NW - 1)
-                            get(xw + kSlotF + (NUP + xch_rank(U, C, 1, XF)) * kCompF, gd, C);
+                    if constexpr (uses_dc(U, C, -1)) {
+#pragma unroll
+                        for (int r = 0; r < R; ++r)
+                            sl[r + 1][C] = __shfl_up_sync(0xffffffffu, v[r][CPT - 1][C], 1);
+                    }
+                    if constexpr (uses_dc(U, C, 1)) {
+#pragma unroll
+                        for (int r = 0; r < R; ++r)
+                            sr[r + 1][C] = __shfl_down_sync(0xffffffffu, v[r][0][C], 1);
+                    }
                 });
-                (void)NDN;
-                xslot ^= 1;
-            }
-            if constexpr (MIRROR) vfix(std::true_type{});
-            sfor<4>([&](auto c_) {
-                constexpr int C = decltype(c_)::value;
-                if constexpr (uses(U, C, -1, -1))
-                    sl[0][C] = __shfl_up_sync(0xffffffffu, gu[CPT - 1][C], 1);
-                if constexpr (uses(U, C, 1, -1))
-                    sl[R + 1][C] = __shfl_up_sync(0xffffffffu, gd[CPT - 1][C], 1);
-                if constexpr (uses(U, C, -1, 1))
-                    sr[0][C] = __shfl_down_sync(0xffffffffu, gu[0][C], 1);
-                if constexpr (uses(U, C, 1, 1))
-                    sr[R + 1][C] = __shfl_down_sync(0xffffffffu, gd[0][C], 1);
-            });
-            if constexpr (MIRROR) hfix(sl, sr, 0, R + 1);  // corners (and rows again)
-            row(std::integral_constant<int, 0>{});
-            row(std::integral_constant<int, R - 1>{});
-#pragma unroll
-            for (int r = 0; r < R; ++r)
-#pragma unroll
-                for (int c = 0; c < CPT; ++c) {
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) v[r][c][k] = o[r][c][k];
-                    P::template post<E>(v[r][c]);
+                if constexpr (MIRROR) hfix(sl, sr, 1, R);
+                float o[R][CPT][4];
+                auto row = [&](auto r_) {
+                    sfor<CPT>([&](auto c_) {
+                        constexpr int RR = decltype(r_)::value, CC = decltype(c_)::value;
+                        Acc<R, CPT, RR, CC> acc{v, gu, gd, sl, sr};
+                        P::template nbr<E>(acc, o[RR][CC]);
+                    });
+                };
+                // interior rows 1..R-2 read only this warp's rows
+                sfor<R - 2>([&](auto r_) { row(std::integral_constant<int, decltype(r_)::value + 1>{}); });
+                if constexpr (E > 0) {
+                    sfor<4>([&](auto c_) {
+                        constexpr int C = decltype(c_)::value;
+                        if constexpr (xch_up(U, C, XF))  // bottom row of the warp above
+                            if (warp > 0) get(xw - kSlotF + xch_rank(U, C, -1, XF) * kCompF, gu, C);
+                        if constexpr (xch_dn(U, C, XF))  // top row of the warp below
+                            if (warp < NW - 1)
+                                get(xw + kSlotF + (NUP + xch_rank(U, C, 1, XF)) * kCompF, gd, C);
+                    });
+                    (void)NDN;
+                    xslot ^= 1;
                 }
-        });
+                if constexpr (MIRROR) vfix(std::true_type{});
+                sfor<4>([&](auto c_) {
+                    constexpr int C = decltype(c_)::value;
+                    if constexpr (uses(U, C, -1, -1))
+                        sl[0][C] = __shfl_up_sync(0xffffffffu, gu[CPT - 1][C], 1);
+                    if constexpr (uses(U, C, 1, -1))
+                        sl[R + 1][C] = __shfl_up_sync(0xffffffffu, gd[CPT - 1][C], 1);
+                    if constexpr (uses(U, C, -1, 1))
+                        sr[0][C] = __shfl_down_sync(0xffffffffu, gu[0][C], 1);
+                    if constexpr (uses(U, C, 1, 1))
+                        sr[R + 1][C] = __shfl_down_sync(0xffffffffu, gd[0][C], 1);
+                });
+                if constexpr (MIRROR) hfix(sl, sr, 0, R + 1);  // corners (and rows again)
+                row(std::integral_constant<int, 0>{});
+                row(std::integral_constant<int, R - 1>{});
+#pragma unroll
+                for (int r = 0; r < R; ++r)
+#pragma unroll
+                    for (int c = 0; c < CPT; ++c) {
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) v[r][c][k] = o[r][c][k];
+                        P::template post<E>(v[r][c]);
+                    }
+            });
 
 #endif  // WL_DIAG_NO_COMPUTE
-        // ---------------- store ----------------
-        const int gy0 = cy + 1 + warp * R;  // global cell row of v[0]
-        const int gx = cx + CPT * lane;     // global cell col of column 0
-        if (DIR == 0 && a.scaling) {  // scale_planes (transform.cpp:154-159)
+            // ---------------- store ----------------
+            const int gy0 = cy + 1 + warp * R;  // global cell row of v[0]
+            const int gx = cx + CPT * lane;     // global cell col of column 0
+            if (DIR == 0 && a.scaling) {  // scale_planes (transform.cpp:154-159)
 #pragma unroll
-            for (int r = 0; r < R; ++r)
+                for (int r = 0; r < R; ++r)
 #pragma unroll
-                for (int c = 0; c < CPT; ++c) {
-                    v[r][c][0] *= a.scale;
-                    v[r][c][3] /= a.scale;
+                    for (int c = 0; c < CPT; ++c) {
+                        v[r][c][0] *= a.scale;
+                        v[r][c][3] /= a.scale;
+                    }
+            }
+            // 64-bit row pointers of the lane's first cell, advanced per row
+            float* pk[4];
+            const long off0 = DIR == 0 ? (long)(gy0 - a.ylo) * a.out_pitch + gx
+                                       : (long)(2 * (gy0 - a.ylo)) * a.out_pitch + 2 * gx;
+#pragma unroll
+            for (int k = 0; k < (DIR == 0 ? 4 : 1); ++k) pk[k] = a.out[k] + b * a.out_bstride[k] + off0;
+            const long step = DIR == 0 ? a.out_pitch : 2 * a.out_pitch;
+            if constexpr (CPT == 4) {
+                // Whole-lane halo (lanes 0 and 31): a lane stores its 4 cells as
+                // one aligned float4 per plane (qw = 0 mod 4, cx = 0 mod 4), or
+                // nothing. Row validity is warp-uniform.
+                const bool c_ok = lane >= HX / 4 && lane < 32 - HX / 4 && gx >= 0 && gx < a.qw;
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const int qr = warp * R + r;
+                    const int gy = gy0 + r;
+#ifdef WL_DIAG_NO_STORE
+                    const bool ok = a.ylo == -777;  // diagnostic: compute only (never true, not DCE-able)
+#else
+                    const bool ok = c_ok && qr >= H && qr < H + a.TH && gy >= a.ylo && gy < a.yhi;
+#endif
+                    if (DIR == 0) {
+#pragma unroll
+                        for (int k = 0; k < 4; ++k)
+                            if (ok)
+                                *reinterpret_cast<float4*>(pk[k] + r * step) =
+                                    make_float4(v[r][0][k], v[r][1][k], v[r][2][k], v[r][3][k]);
+                    } else {
+                        float* p0 = pk[0] + r * step;
+                        float* p1 = p0 + a.out_pitch;
+                        if (ok) {
+                            *reinterpret_cast<float4*>(p0) =
+                                make_float4(v[r][0][0], v[r][0][1], v[r][1][0], v[r][1][1]);
+                            *reinterpret_cast<float4*>(p0 + 4) =
+                                make_float4(v[r][2][0], v[r][2][1], v[r][3][0], v[r][3][1]);
+                            *reinterpret_cast<float4*>(p1) =
+                                make_float4(v[r][0][2], v[r][0][3], v[r][1][2], v[r][1][3]);
+                            *reinterpret_cast<float4*>(p1 + 4) =
+                                make_float4(v[r][2][2], v[r][2][3], v[r][3][2], v[r][3][3]);
+                        }
+                    }
                 }
-        }
-        // 64-bit row pointers of the lane's first cell, advanced per row
-        float* pk[4];
-        const long off0 = DIR == 0 ? (long)(gy0 - a.ylo) * a.out_pitch + gx
-                                   : (long)(2 * (gy0 - a.ylo)) * a.out_pitch + 2 * gx;
-#pragma unroll
-        for (int k = 0; k < (DIR == 0 ? 4 : 1); ++k) pk[k] = a.out[k] + b * a.out_bstride[k] + off0;
-        const long step = DIR == 0 ? a.out_pitch : 2 * a.out_pitch;
-        if constexpr (CPT == 4) {
-            // Whole-lane halo (lanes 0 and 31): a lane stores its 4 cells as
-            // one aligned float4 per plane (qw = 0 mod 4, cx = 0 mod 4), or
-            // nothing. Row validity is warp-uniform.
-            const bool c_ok = lane >= HX / 4 && lane < 32 - HX / 4 && gx >= 0 && gx < a.qw;
+            } else {
+            // output columns of this tile, clipped to the image (partial tiles)
+            const bool c0 = CPT * lane >= H && CPT * lane < H + a.TW && gx >= 0 && gx < a.qw;
+            const bool c1 =
+                CPT * lane + 1 >= H && CPT * lane + 1 < H + a.TW && gx + 1 >= 0 && gx + 1 < a.qw;
+            // Branch-free, predicated stores: both cells (vector store) / only
+            // the left / only the right cell. Row validity is warp-uniform.
+            // With an even halo a lane's two cells are both stored or both halo
+            // (only the "both" store exists); odd halos also need single cells.
+            constexpr bool kPairs = WL_STORE_PAIRS && (H % 2 == 0);
+            const bool both = c0 && c1, only0 = !kPairs && c0 && !c1, only1 = !kPairs && c1 && !c0;
 #pragma unroll
             for (int r = 0; r < R; ++r) {
                 const int qr = warp * R + r;
                 const int gy = gy0 + r;
-#ifdef WL_DIAG_NO_STORE
-                const bool ok = a.ylo == -777;  // diagnostic: compute only (never true, not DCE-able)
-#else
-                const bool ok = c_ok && qr >= H && qr < H + a.TH && gy >= a.ylo && gy < a.yhi;
-#endif
+                const bool row_ok = qr >= H && qr < H + a.TH && gy >= a.ylo && gy < a.yhi;
                 if (DIR == 0) {
 #pragma unroll
-                    for (int k = 0; k < 4; ++k)
-                        if (ok)
-                            *reinterpret_cast<float4*>(pk[k] + r * step) =
-                                make_float4(v[r][0][k], v[r][1][k], v[r][2][k], v[r][3][k]);
+                    for (int k = 0; k < 4; ++k) {
+                        float* p = pk[k] + r * step;
+                        if (row_ok && both)
+                            *reinterpret_cast<float2*>(p) = make_float2(v[r][0][k], v[r][1][k]);
+                        if (row_ok && only0) p[0] = v[r][0][k];
+                        if (row_ok && only1) p[1] = v[r][1][k];
+                    }
                 } else {
                     float* p0 = pk[0] + r * step;
                     float* p1 = p0 + a.out_pitch;
-                    if (ok) {
+                    if (row_ok && both) {
                         *reinterpret_cast<float4*>(p0) =
                             make_float4(v[r][0][0], v[r][0][1], v[r][1][0], v[r][1][1]);
-                        *reinterpret_cast<float4*>(p0 + 4) =
-                            make_float4(v[r][2][0], v[r][2][1], v[r][3][0], v[r][3][1]);
                         *reinterpret_cast<float4*>(p1) =
                             make_float4(v[r][0][2], v[r][0][3], v[r][1][2], v[r][1][3]);
-                        *reinterpret_cast<float4*>(p1 + 4) =
-                            make_float4(v[r][2][2], v[r][2][3], v[r][3][2], v[r][3][3]);
+                    }
+                    if (row_ok && only0) {
+                        *reinterpret_cast<float2*>(p0) = make_float2(v[r][0][0], v[r][0][1]);
+                        *reinterpret_cast<float2*>(p1) = make_float2(v[r][0][2], v[r][0][3]);
+                    }
+                    if (row_ok && only1) {
+                        *reinterpret_cast<float2*>(p0 + 2) = make_float2(v[r][1][0], v[r][1][1]);
+                        *reinterpret_cast<float2*>(p1 + 2) = make_float2(v[r][1][2], v[r][1][3]);
                     }
                 }
             }
-        } else {
-        // output columns of this tile, clipped to the image (partial tiles)
-        const bool c0 = CPT * lane >= H && CPT * lane < H + a.TW && gx >= 0 && gx < a.qw;
-        const bool c1 =
-            CPT * lane + 1 >= H && CPT * lane + 1 < H + a.TW && gx + 1 >= 0 && gx + 1 < a.qw;
-        // Branch-free, predicated stores: both cells (vector store) / only
-        // the left / only the right cell. Row validity is warp-uniform.
-        // With an even halo a lane's two cells are both stored or both halo
-        // (only the "both" store exists); odd halos also need single cells.
-        constexpr bool kPairs = WL_STORE_PAIRS && (H % 2 == 0);
-        const bool both = c0 && c1, only0 = !kPairs && c0 && !c1, only1 = !kPairs && c1 && !c0;
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-            const int qr = warp * R + r;
-            const int gy = gy0 + r;
-            const bool row_ok = qr >= H && qr < H + a.TH && gy >= a.ylo && gy < a.yhi;
-            if (DIR == 0) {
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    float* p = pk[k] + r * step;
-                    if (row_ok && both)
-                        *reinterpret_cast<float2*>(p) = make_float2(v[r][0][k], v[r][1][k]);
-                    if (row_ok && only0) p[0] = v[r][0][k];
-                    if (row_ok && only1) p[1] = v[r][1][k];
-                }
-            } else {
-                float* p0 = pk[0] + r * step;
-                float* p1 = p0 + a.out_pitch;
-                if (row_ok && both) {
-                    *reinterpret_cast<float4*>(p0) =
-                        make_float4(v[r][0][0], v[r][0][1], v[r][1][0], v[r][1][1]);
-                    *reinterpret_cast<float4*>(p1) =
-                        make_float4(v[r][0][2], v[r][0][3], v[r][1][2], v[r][1][3]);
-                }
-                if (row_ok && only0) {
-                    *reinterpret_cast<float2*>(p0) = make_float2(v[r][0][0], v[r][0][1]);
-                    *reinterpret_cast<float2*>(p1) = make_float2(v[r][0][2], v[r][0][3]);
-                }
-                if (row_ok && only1) {
-                    *reinterpret_cast<float2*>(p0 + 2) = make_float2(v[r][1][0], v[r][1][1]);
-                    *reinterpret_cast<float2*>(p1 + 2) = make_float2(v[r][1][2], v[r][1][3]);
-                }
+            }  // CPT == 2
+            if constexpr (FUSED) {  // this warp's stores of tile i-1 are issued: count it
+                __syncwarp();
+                if (lane == 0)
+                    asm volatile("red.release.cta.shared.add.u32 [%0], 1;" ::"r"(
+                                     smem_u32(&done_cnt[(i - 1) & (kRing - 1)]))
+                                 : "memory");
             }
+        };
+        if constexpr (FUSED) {
+            if (lvl) body(std::integral_constant<int, 1>{});
+            else body(std::integral_constant<int, 0>{});
+        } else {
+            body(std::integral_constant<int, 0>{});
         }
-        }  // CPT == 2
     }
 }
 
@@ -1111,12 +1415,13 @@ inline Plan plan_tiles(const WlLevel& L, int H, int R, int NW, int CPT) {
     return p;
 }
 
-template <class P, int DIR, int R, int NW, int CPT, int NS, bool XF, int MAXB>
-cudaError_t launch(const WlLevel& L, const Plan& plan, cudaStream_t stream) {
+// Kernel arguments and tensor maps of one level (shared by launch and
+// launch_fused).
+template <class P, int DIR, int R, int NW, int CPT, int NS, bool XF>
+bool level_args(const WlLevel& L, const Plan& plan, FastArgs& a, CUtensorMap (&maps)[4]) {
     using G = Geometry<R, NW, CPT, NS, xch_comps<P, XF>()>;
     constexpr int TWC = G::TWC;
-    CUtensorMap maps[4];
-    FastArgs a = plan.args;
+    a = plan.args;
     const int nb = L.nb > 1 ? L.nb : 1;
     for (int k = 0; k < 4; ++k) {
         a.in_bstride[k] = nb > 1 ? L.in_bstride[k] : 0;
@@ -1126,14 +1431,14 @@ cudaError_t launch(const WlLevel& L, const Plan& plan, cudaStream_t stream) {
         static_assert((2 * G::kRows) % WL_FWD_SPLIT == 0, "split must divide the tile rows");
         if (!make_map(&maps[0], L.in[0], 2 * L.qw, 2 * L.qh, L.in_pitch, nb, a.in_bstride[0],
                       2 * TWC, 2 * G::kRows / WL_FWD_SPLIT))
-            return cudaErrorInvalidValue;
+            return false;
         maps[1] = maps[2] = maps[3] = maps[0];
         for (int k = 0; k < 4; ++k) a.out[k] = L.out[k];
     } else {
         for (int k = 0; k < 4; ++k)
             if (!make_map(&maps[k], L.in[k], L.qw, L.qh, L.in_pitch, nb, a.in_bstride[k], TWC,
                           G::kRows))
-                return cudaErrorInvalidValue;
+                return false;
         a.out[0] = L.out[0];
         a.out[1] = a.out[2] = a.out[3] = nullptr;
     }
@@ -1146,43 +1451,141 @@ cudaError_t launch(const WlLevel& L, const Plan& plan, cudaStream_t stream) {
     a.out_pitch = L.out_pitch;
     a.scaling = L.scaling && wl_host_program(L.prog).has_scale;
     a.scale = wl_host_program(L.prog).scale;
+    return true;
+}
+
+// Persistent grid size of a kernel variant: SMs x resident CTAs (cached per device).
+template <int R, int NW, int CPT, int NS, int NXC, int MAXB, class Kern>
+int grid_cap(Kern kern, int* cache) {
+    using G = Geometry<R, NW, CPT, NS, NXC>;
     int dev = 0;
     cudaGetDevice(&dev);
-    // grid cap per kernel variant: persistent CTAs = SMs x resident CTAs
-    auto cap_of = [&](auto kern, int* cache) {
-        int& mb = cache[dev & 63];
-        if (mb != 0) return mb;
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)G::kSmemBytes);
-        int per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (NW + 1) * 32,
-                                                      G::kSmemBytes);
-        int sms = 0;
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (MAXB > 0 && per_sm > MAXB) per_sm = MAXB;
-        mb = (per_sm > 0 ? per_sm : 1) * sms;
-        if (getenv("WL_VERBOSE"))
-            fprintf(stderr, "[wl] fast_kernel R=%d NW=%d CPT=%d NS=%d smem=%zu B: %d CTA/SM\n", R,
-                    NW, CPT, NS, (size_t)G::kSmemBytes, per_sm);
-        return mb;
-    };
+    int& mb = cache[dev & 63];
+    if (mb != 0) return mb;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::kSmemBytes);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (NW + 1) * 32, G::kSmemBytes);
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (MAXB > 0 && per_sm > MAXB) per_sm = MAXB;
+    mb = (per_sm > 0 ? per_sm : 1) * sms;
+    if (getenv("WL_VERBOSE"))
+        fprintf(stderr, "[wl] fast_kernel R=%d NW=%d CPT=%d NS=%d smem=%zu B: %d CTA/SM\n", R, NW,
+                CPT, NS, (size_t)G::kSmemBytes, per_sm);
+    return mb;
+}
+
+template <class P, int DIR, int R, int NW, int CPT, int NS, bool XF, int MAXB>
+cudaError_t launch(const WlLevel& L, const Plan& plan, cudaStream_t stream) {
+    constexpr int NXC = xch_comps<P, XF>();
+    using G = Geometry<R, NW, CPT, NS, NXC>;
+    CUtensorMap maps[4];
+    KArgs k{};
+    if (!level_args<P, DIR, R, NW, CPT, NS, XF>(L, plan, k.lv[0], maps))
+        return cudaErrorInvalidValue;
     static int cap_norm[64] = {}, cap_mirr[64] = {};
     auto run = [&](auto kern, int* cache, int filter) -> cudaError_t {
-        const int mb = cap_of(kern, cache);
-        FastArgs f = a;
-        f.filter = filter;
-        const int grid = f.ntiles < mb ? f.ntiles : mb;
+        const int mb = grid_cap<R, NW, CPT, NS, NXC, MAXB>(kern, cache);
+        KArgs f = k;
+        f.lv[0].filter = filter;
+        const int grid = f.lv[0].ntiles < mb ? f.lv[0].ntiles : mb;
         cudaError_t le = launch_pdl(kern, dim3(grid), dim3((NW + 1) * 32), G::kSmemBytes,
                                     stream, maps[0], maps[1], maps[2], maps[3], f);
         wl_count_launch();
         return le != cudaSuccess ? le : cudaGetLastError();
     };
-    if (!a.mirror) return run(fast_kernel<P, DIR, R, NW, CPT, NS, XF, false>, cap_norm, 0);
+    if (!k.lv[0].mirror) return run(fast_kernel<P, DIR, R, NW, CPT, NS, XF, false>, cap_norm, 0);
     // symmetric whole-image plan: interior tiles on the plain kernel, the ring
     // of border tiles on the mirroring variant (same grid, disjoint tiles)
     cudaError_t e = run(fast_kernel<P, DIR, R, NW, CPT, NS, XF, false>, cap_norm, 1);
     if (e != cudaSuccess) return e;
     return run(fast_kernel<P, DIR, R, NW, CPT, NS, XF, true>, cap_mirr, 2);
+}
+
+// Fused launch of two consecutive periodic forward levels (L1 reads L0's LL
+// output). `ctr` = fused_ctr_elems(...) zeroed words on the stream (memset
+// here). Returns cudaErrorNotSupported when the pair does not qualify.
+inline int fused_ready_c(const Plan& p0, const Plan& p1, int H, int kRows) {
+    // smallest c with ready(k) = min(2k+1+c, R0-1) >= the last level-l tile
+    // row every level-(l+1) tile row k >= 1 reads (k = 0 wraps: last anyway)
+    const FastArgs& a0 = p0.args;
+    const FastArgs& a1 = p1.args;
+    const int R0 = p0.tiles_y, R1 = p1.tiles_y, qh0 = a0.qh;
+    auto fdiv = [](int x, int y) { return x >= 0 ? x / y : -((-x + y - 1) / y); };
+    int c = 0;
+    for (int k = 1; k < R1; ++k) {
+        const int cy = a1.Y0 + (k + a1.ty0) * a1.TH - H - 1;
+        const int ya = 2 * cy, yb = 2 * (cy + kRows);
+        int need;
+        if (ya < 0 || yb > qh0) need = R0 - 1;  // wraps: needs the last row
+        else need = fdiv(yb - 1 - a0.Y0, a0.TH) - a0.ty0;
+        if (need > R0 - 1) need = R0 - 1;
+        while (std::min(2 * k + 1 + c, R0 - 1) < need) ++c;
+    }
+    return c;
+}
+
+template <class P, int DIR, int R, int NW, int CPT, int NS, bool XF, int MAXB>
+cudaError_t launch_fused(const WlLevel& L0, const Plan& p0, const WlLevel& L1, const Plan& p1,
+                         unsigned* ctr, cudaStream_t stream) {
+    if constexpr (DIR != 0) {
+        return cudaErrorNotSupported;
+    } else {
+        constexpr int NXC = xch_comps<P, XF>();
+        using G = Geometry<R, NW, CPT, NS, NXC>;
+        CUtensorMap maps0[4], maps1[4];
+        KArgs k{};
+        if (!level_args<P, DIR, R, NW, CPT, NS, XF>(L0, p0, k.lv[0], maps0) ||
+            !level_args<P, DIR, R, NW, CPT, NS, XF>(L1, p1, k.lv[1], maps1))
+            return cudaErrorInvalidValue;
+        if (k.lv[0].mirror || k.lv[1].mirror || !k.lv[0].wrap || !k.lv[1].wrap ||
+            k.lv[0].Y0 != k.lv[1].Y0 || k.lv[0].TH != k.lv[1].TH || k.lv[0].ty0 != k.lv[1].ty0)
+            return cudaErrorNotSupported;
+        FuseArgs& f = k.fu;
+        const int nb = L0.nb > 1 ? L0.nb : 1;
+        f.ctr = ctr;
+        f.nb = nb;
+        f.R0 = p0.tiles_y;
+        f.R1 = p1.tiles_y;
+        f.X0n = p0.args.tiles_x;
+        f.X1n = p1.args.tiles_x;
+        f.c = fused_ready_c(p0, p1, P::kHalo, G::kRows);
+        const long per_img = (long)f.R0 * f.X0n + (long)f.R1 * f.X1n;
+        if ((long)nb * per_img >= (1l << 30) || (long)nb * f.R0 >= (1l << 30))
+            return cudaErrorNotSupported;
+        f.ntasks = (int)(nb * per_img);
+        static const int diag = [] {  // timing diagnostic: 1 = level-l tiles only
+            const char* v = getenv("WL_FUSE_DIAG");
+            return v ? atoi(v) : 0;
+        }();
+        if (diag == 1) {
+            f.R1 = 0;
+            f.ntasks = nb * f.R0 * f.X0n;
+        }
+        f.target = (unsigned)f.X0n * NW;
+        static int cap[64] = {};
+        auto kern = fast_kernel<P, DIR, R, NW, CPT, NS, XF, false, true>;
+        const int mb = grid_cap<R, NW, CPT, NS, NXC, MAXB>(kern, cap);
+        const int grid = f.ntasks < mb ? f.ntasks : mb;
+        // lag: the tasks claimed but possibly unfinished (grid x stages), in
+        // level-l rows of the sequence (X0n + X1n/2 tasks each), plus one
+        {
+            static const int dmul = [] {
+                const char* v = getenv("WL_FUSE_LAG");
+                return v ? atoi(v) : 150;
+            }();
+            const int per_row = f.X0n + (f.X1n + 1) / 2;
+            const long inflight = (long)grid * (NS + 2 * WL_FUSE_CLAIM);
+            f.D = (int)((inflight * dmul / 100 + per_row - 1) / per_row) + 1;
+        }
+        cudaError_t e = cudaMemsetAsync(ctr, 0, (1 + (size_t)nb * f.R0) * sizeof(unsigned), stream);
+        if (e != cudaSuccess) return e;
+        // maps: m0 = level-l image, m1 = level-(l+1) input (= LL_l)
+        cudaError_t le = launch_pdl(kern, dim3(grid), dim3((NW + 1) * 32), G::kSmemBytes, stream,
+                                    maps0[0], maps1[0], maps0[0], maps0[0], k);
+        wl_count_launch();
+        return le != cudaSuccess ? le : cudaGetLastError();
+    }
 }
 
 }  // namespace wlfast

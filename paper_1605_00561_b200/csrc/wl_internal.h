@@ -58,6 +58,12 @@ cudaError_t wl_launch_conv_fast(const WlLevel& L, cudaStream_t stream);
 // (wavelet, scheme, direction) has no fast instantiation.
 cudaError_t wl_launch_fast(const WlLevel& L, cudaStream_t stream);
 bool wl_fast_supported(const WlLevel& L);
+// Two consecutive periodic forward pyramid levels (L1 reads L0's LL) in one
+// persistent launch; cudaErrorNotSupported when the pair does not qualify
+// (then launch them one by one). `ctr`: wl_fused_ctr_elems(L0.qh, nb) words.
+size_t wl_fused_ctr_elems(int qh0, int nb);
+cudaError_t wl_launch_fast_fused(const WlLevel& L0, const WlLevel& L1, unsigned* ctr,
+                                 cudaStream_t stream);
 
 void wl_count_launch();
 // Records `msg` as this thread's wl_last_error() and returns `code`.
