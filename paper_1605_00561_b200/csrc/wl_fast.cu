@@ -167,7 +167,7 @@ cudaError_t wl_launch_fast(const WlLevel& L, cudaStream_t stream) {
 }
 
 size_t wl_fused_ctr_elems(int qh0, int nb) {
-    // 1 + nb * R0 words; R0 <= qh0 / TH + 3 with TH >= 22 for every forward geometry
+    // 2 + nb * R0 words; R0 <= qh0 / TH + 3 with TH >= 22 for every forward geometry
     return 16 + static_cast<size_t>(nb > 1 ? nb : 1) * (qh0 / 16 + 4);
 }
 
@@ -188,7 +188,7 @@ cudaError_t wl_launch_fast_fused(const WlLevel& L0, const WlLevel& L1, unsigned*
     const wlfast::Plan p1 = wlfast::plan_tiles(L1, H, R, NW, CPT);
     if (!p0.ok || !p1.ok) return cudaErrorNotSupported;
     const int nb = L0.nb > 1 ? L0.nb : 1;
-    if (1 + static_cast<size_t>(nb) * p0.tiles_y > wl_fused_ctr_elems(L0.qh, nb))
+    if (2 + static_cast<size_t>(nb) * p0.tiles_y > wl_fused_ctr_elems(L0.qh, nb))
         return cudaErrorNotSupported;
     return L0.wavelet == 0 ? wl_fast_cdf53_fwd_fused(L0.scheme, L0, p0, L1, p1, ctr, stream)
                            : wl_fast_cdf97_fwd_fused(L0.scheme, L0, p0, L1, p1, ctr, stream);

@@ -264,28 +264,23 @@ __device__ inline void wait_halo_flags(const unsigned* fa, const unsigned* fb, u
     asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
-// Two pyramid levels in ONE persistent launch (forward, periodic): the tiles
-// of level l and of level l+1 form one task sequence over the whole batch --
-// level-l tile rows in order (global row J = b*R0 + j), each followed by the
-// level-(l+1) tile rows that become ready with it. Level-(l+1) row k of
-// image b reads LL_l rows held by level-l rows <= 2k+1+c of that image (the
-// wrapping top row k = 0 needs the image's last row and goes last); it is
-// emitted D rows later than that (D covers the tasks CTAs have claimed but
-// not finished, so its producer rarely waits). CTAs claim tasks in sequence
-// order from a global counter (ctr[0]); a level-l tile's warps count their
-// completion per tile row (ctr[1 + b*R0 + j], release); a level-(l+1) tile's
-// producer waits (acquire) for the rows of LL_l its TMA box covers.
-// Dependencies always point to earlier tasks and tasks are claimed in
-// order, so the wait cannot deadlock. LL_l is re-read while still in L2.
+// Two pyramid levels in ONE persistent launch (forward, periodic). Level-l
+// tiles and level-(l+1) tiles are two task queues (global counters ctr[0],
+// ctr[1], claimed in order). Level-l tiles never wait. A level-(l+1) tile
+// reads LL_l rows that level-l tiles write: each CTA's producer keeps the
+// next level-(l+1) task it claimed pending and takes it as soon as the
+// level-l tile rows its TMA box covers are complete (per-row counts
+// ctr[2 + b*R0 + j]), processing level-l tiles meanwhile -- so LL_l is
+// re-read right after it was written, from L2, and nobody idles while
+// level-l tiles remain (then the pending task is waited for). No cycle:
+// level-l tiles depend on nothing.
 struct FuseArgs {
-    unsigned* ctr;  // [0] task counter, [1 + b*R0 + j] warps done with level-l row j
+    unsigned* ctr;  // [0] level-l claims, [1] level-(l+1) claims, [2 + b*R0 + j] row counts
     int nb;         // images
     int R0, R1;     // tile rows per image of level l / l+1
     int X0n, X1n;   // tile columns
-    int c;          // level-(l+1) row k (k >= 1) needs level-l rows <= 2k+1+c
-    int D;          // emission lag in level-l rows
-    int ntasks;
-    unsigned target;  // ctr value of a finished level-l tile row (X0n * NW)
+    int n0, n1;     // tasks per level (all images)
+    unsigned target;  // row count of a finished level-l tile row (X0n * NW)
 };
 struct KArgs {
     FastArgs lv[2];  // lv[1]: the second level of a fused launch
@@ -294,57 +289,6 @@ struct KArgs {
 
 __device__ __host__ __forceinline__ int floordiv(int a, int b) {
     return a >= 0 ? a / b : -((-a + b - 1) / b);
-}
-// Level-(l+1) rows emitted up to and including global level-l row J
-// (list order per image: k = 1..R1-1, then 0).
-__device__ __host__ __forceinline__ int fused_n1(const FuseArgs& f, int J) {
-    if (J >= f.nb * f.R0 - 1) return f.nb * f.R1;
-    if (J < 0 || f.R1 == 0) return 0;
-    // images whose rows are all emitted: J - b*R0 - D >= R0 - 1
-    int bf = floordiv(J - f.D - f.R0 + 1, f.R0) + 1;
-    bf = bf < 0 ? 0 : (bf > f.nb ? f.nb : bf);
-    int n = bf * f.R1;
-    if (bf < f.nb) {  // the one partially emitted image
-        const int jj = J - bf * f.R0 - f.D;
-        if (jj >= 0) {
-            const int v = floordiv(jj - 1 - f.c, 2);  // rows k = 1..v
-            n += v < 0 ? 0 : (v > f.R1 - 1 ? f.R1 - 1 : v);
-        }
-    }
-    return n;
-}
-// Task t -> (level, image, tile row, tile column) of a fused launch.
-__device__ __forceinline__ void fused_decode(const FuseArgs& f, int t, int& lvl, int& b, int& tyi,
-                                             int& txi, int& row_end) {
-    auto cum = [&](int J) { return (J + 1) * f.X0n + fused_n1(f, J) * f.X1n; };
-    // smallest J with cum(J) > t: estimate from the steady state (a level-l
-    // row plus half a level-(l+1) row per step, D + 1 + c rows of lag), then
-    // correct (image ends shift it by a few rows)
-    const int last = f.nb * f.R0 - 1;
-    const float x1 = f.R1 > 0 ? (float)f.X1n : 0.f;
-    int lo = (int)(((float)t + 0.5f * (float)(f.D + 1 + f.c) * x1) /
-                   ((float)f.X0n + x1 * (float)f.R1 / (float)f.R0));
-    lo = lo < 0 ? 0 : (lo > last ? last : lo);
-    while (lo > 0 && cum(lo - 1) > t) --lo;
-    while (lo < last && cum(lo) <= t) ++lo;
-    int r = t - (lo > 0 ? cum(lo - 1) : 0);
-    if (r < f.X0n) {
-        lvl = 0;
-        b = lo / f.R0;
-        tyi = lo - b * f.R0;
-        txi = r;
-        row_end = t - r + f.X0n;
-    } else {
-        r -= f.X0n;
-        const int m = r / f.X1n;
-        const int g = fused_n1(f, lo - 1) + m;  // global level-(l+1) list index
-        lvl = 1;
-        b = g / f.R1;
-        const int i = g - b * f.R1;
-        tyi = i + 1 < f.R1 ? i + 1 : 0;
-        txi = r - m * f.X1n;
-        row_end = t - txi + f.X1n;
-    }
 }
 __device__ __forceinline__ unsigned ld_acquire_gpu_u32(const unsigned* p) {
     unsigned v;
@@ -356,17 +300,15 @@ __device__ __forceinline__ unsigned ld_relaxed_gpu_u32(const unsigned* p) {
     asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
-// Producer of a level-(l+1) tile: wait until the level-l tile rows holding
-// LL_l rows [2*cy, 2*(cy + rows)) (wrapped) are complete. The (at most a
-// few) row counters are polled with independent loads -- one round trip per
-// poll -- and one acquire fence follows; `known` caches the last verified
-// row range of an image (tiles of one level-(l+1) row share it).
+// Producer of a level-(l+1) tile: are the level-l tile rows holding LL_l
+// rows [2*cy, 2*(cy + rows)) (wrapped) complete? One poll of the (few) row
+// counts with independent loads; on success one acquire fence (plus the
+// generic -> async proxy fence: the tile is read by TMA). `known` caches the
+// last verified row range of an image (tiles of one row share it).
 struct RowCache {
     int b = -1, lo = 0, hi = -1;
 };
-template <class Idle>
-__device__ inline void fused_wait_rows(const KArgs& K, int b, int cy, int rows, RowCache& known,
-                                       Idle&& idle) {
+__device__ inline bool fused_rows_ready(const KArgs& K, int b, int cy, int rows, RowCache& known) {
     const FastArgs& a0 = K.lv[0];
     const FuseArgs& f = K.fu;
     const int qh0 = a0.qh;
@@ -387,20 +329,12 @@ __device__ inline void fused_wait_rows(const KArgs& K, int b, int cy, int rows, 
             hi1 = jof(y1);
         }
     }
-    if (hi1 < 0 && known.b == b && lo0 >= known.lo && hi0 <= known.hi) return;
-    const unsigned* c = f.ctr + 1 + (size_t)b * f.R0;
-    unsigned ns = 32;
-    for (;;) {
-        bool ok = true;
-        for (int j = lo0; j <= hi0; ++j) ok &= ld_relaxed_gpu_u32(c + j) >= f.target;
-        for (int j = lo1; j <= hi1; ++j) ok &= ld_relaxed_gpu_u32(c + j) >= f.target;
-        if (ok) break;
-        idle();  // report this CTA's own finished rows: they may be the ones missing
-        __nanosleep(ns);
-        ns = ns < 256 ? 2 * ns : 256;
-    }
-    // acquire the rows' data; LL_l was written by generic stores and the
-    // tile is read by TMA (async proxy)
+    if (hi1 < 0 && known.b == b && lo0 >= known.lo && hi0 <= known.hi) return true;
+    const unsigned* c = f.ctr + 2 + (size_t)b * f.R0;
+    bool ok = true;
+    for (int j = lo0; j <= hi0; ++j) ok &= ld_relaxed_gpu_u32(c + j) >= f.target;
+    for (int j = lo1; j <= hi1; ++j) ok &= ld_relaxed_gpu_u32(c + j) >= f.target;
+    if (!ok) return false;
     asm volatile("fence.acq_rel.gpu;" ::: "memory");
     asm volatile("fence.proxy.async.global;" ::: "memory");
     if (hi1 < 0) {
@@ -408,6 +342,31 @@ __device__ inline void fused_wait_rows(const KArgs& K, int b, int cy, int rows, 
         known.lo = lo0;
         known.hi = hi0;
     }
+    return true;
+}
+
+// The (at most kMaxDep) level-l tile rows a level-(l+1) box covers.
+constexpr int kMaxDep = 6;
+__device__ inline int fused_dep_rows(const KArgs& K, int cy, int rows, int (&j)[kMaxDep]) {
+    const FastArgs& a0 = K.lv[0];
+    const int qh0 = a0.qh, R0 = K.fu.R0;
+    const int ya = 2 * cy, yb = 2 * (cy + rows);
+    auto jof = [&](int y) { return floordiv(y - a0.Y0, a0.TH) - a0.ty0; };
+    int n = 0;
+    auto add = [&](int lo, int hi) {
+        for (int q = lo; q <= hi && n < kMaxDep; ++q) j[n++] = q;
+    };
+    if (yb - ya >= qh0) return -1;  // the whole image (tiny levels)
+    const int y0 = ((ya % qh0) + qh0) % qh0, y1 = (((yb - 1) % qh0) + qh0) % qh0;
+    if (y0 <= y1) {
+        if (jof(y1) - jof(y0) >= kMaxDep) return -1;
+        add(jof(y0), jof(y1));
+    } else {
+        if (R0 - jof(y0) + jof(y1) + 1 > kMaxDep) return -1;
+        add(jof(y0), R0 - 1);
+        add(0, jof(y1));
+    }
+    return n;
 }
 
 template <int R, int NW, int CPT, int NS = 2, int NXC = 4>
@@ -544,18 +503,16 @@ __global__ void __launch_bounds__((NW + 1) * 32,
     if (warp == NW) {
         // ---------------- producer warp: TMA tile stream ----------------
         if (FUSED && lane == 0) {
-            // Tasks are claimed in chunks of kClaim, the next chunk one chunk
-            // ahead, so the claim's round trip never stalls the TMA stream.
+            const FuseArgs& f = K.fu;
+            // Level-l tasks are claimed in chunks of kClaim, the next chunk one
+            // chunk ahead (the claim's round trip never stalls the TMA stream);
+            // level-(l+1) tasks one at a time, also one ahead.
             constexpr int kClaim = WL_FUSE_CLAIM;
-#ifdef WL_FUSE_STATIC  // diagnostic: static round-robin chunks (no dependency-safe order!)
-            int base = blockIdx.x * kClaim, k_in = 0;
-            int next = base + gridDim.x * kClaim;
-#else
-            int base = atomicAdd(K.fu.ctr, kClaim), k_in = 0;
-            int next = atomicAdd(K.fu.ctr, kClaim);
-#endif
+            int base = atomicAdd(f.ctr, kClaim), k_in = 0;
+            int next = atomicAdd(f.ctr, kClaim);
+            int p1 = atomicAdd(f.ctr + 1, 1);   // pending level-(l+1) task
+            int p1n = atomicAdd(f.ctr + 1, 1);  // the one after it
             RowCache known;
-            int lvl = 0, b = 0, tyi = 0, txi = 0, row_end = -1, prev = -2;
             // Completion reports of level-l tile rows: the compute warps count
             // their finished stores per tile in shared memory (release.cta);
             // this thread turns them, in order, into per-row global counts
@@ -567,7 +524,7 @@ __global__ void __launch_bounds__((NW + 1) * 32,
                 if (prow >= 0) {
                     asm volatile("fence.acq_rel.gpu;" ::: "memory");
                     asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(
-                                     K.fu.ctr + 1 + prow), "r"(pcnt) : "memory");
+                                     f.ctr + 2 + prow), "r"(pcnt) : "memory");
                     prow = -1;
                     pcnt = 0;
                 }
@@ -594,10 +551,6 @@ __global__ void __launch_bounds__((NW + 1) * 32,
                 }
             };
             int issued = 0;
-            auto idle = [&]() {
-                report(issued, false);
-                flush();
-            };
             auto wait_empty = [&](int s_, unsigned ph) {
                 unsigned ns = 32;
                 for (int polls = 0; !mbar_test(&empty[s_], ph); ++polls) {
@@ -607,11 +560,87 @@ __global__ void __launch_bounds__((NW + 1) * 32,
                     ns = ns < WL_PROD_BACKOFF_NS ? 2 * ns : WL_PROD_BACKOFF_NS;
                 }
             };
+            // level-(l+1) task -> image, tile row (list order k = 1..R1-1, 0), column, box row
+            const FastArgs& a1 = K.lv[1];
+            auto decode1 = [&](int t1, int& b_, int& k_, int& tx_, int& cy_) {
+                const int per = f.R1 * f.X1n;
+                b_ = t1 / per;
+                const int r = t1 - b_ * per, i1 = r / f.X1n;
+                k_ = i1 + 1 < f.R1 ? i1 + 1 : 0;
+                tx_ = r - i1 * f.X1n;
+                cy_ = a1.Y0 + (k_ + a1.ty0) * a1.TH - H - 1;
+            };
+            int pb = 0, pk = 0, ptx = 0, pcy = 0;
+            // the pending task's row counts are loaded one iteration ahead
+            // (their round trip overlaps the TMA issue and the stage wait)
+            int pj[kMaxDep], pn = 0;
+            unsigned pv[kMaxDep];
+            auto set_pending = [&]() {
+                decode1(p1, pb, pk, ptx, pcy);
+                pn = fused_dep_rows(K, pcy, G::kRows, pj);
+            };
+            auto prefetch = [&]() {
+                const unsigned* c = f.ctr + 2 + (size_t)pb * f.R0;
+#pragma unroll
+                for (int q = 0; q < kMaxDep; ++q)
+                    if (q < pn) pv[q] = ld_relaxed_gpu_u32(c + pj[q]);
+            };
+            auto prefetched_ready = [&]() {
+                if (pn < 0) return fused_rows_ready(K, pb, pcy, G::kRows, known);
+                bool ok = true;
+#pragma unroll
+                for (int q = 0; q < kMaxDep; ++q)
+                    if (q < pn) ok &= pv[q] >= f.target;
+                if (ok) {
+                    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                    asm volatile("fence.proxy.async.global;" ::: "memory");
+                }
+                return ok;
+            };
+            if (p1 < f.n1) {
+                set_pending();
+                prefetch();
+            }
             for (int i = 0;; ++i) {
-                const int t = base + k_in;
                 const int s = i % NS;
                 const unsigned use = i / NS;
-                if (t >= K.fu.ntasks) {
+                int lvl, b, tyi, txi;
+                const int t0 = base + k_in;
+                bool take1 = p1 < f.n1 && prefetched_ready();
+                if (!take1 && t0 >= f.n0 && p1 < f.n1) {
+                    // no level-l work left: wait for the pending task's rows
+                    unsigned ns = 32;
+                    while (!fused_rows_ready(K, pb, pcy, G::kRows, known)) {
+                        report(issued, false);  // this CTA's own rows may be missing
+                        flush();
+                        __nanosleep(ns);
+                        ns = ns < 256 ? 2 * ns : 256;
+                    }
+                    take1 = true;
+                }
+                if (take1) {
+                    lvl = 1;
+                    b = pb;
+                    tyi = pk;
+                    txi = ptx;
+                    p1 = p1n;
+                    if (p1 < f.n1) {
+                        set_pending();
+                        p1n = atomicAdd(f.ctr + 1, 1);
+                    }
+                } else if (t0 < f.n0) {
+                    lvl = 0;
+                    const int per = f.R0 * f.X0n;
+                    b = t0 / per;
+                    const int r = t0 - b * per;
+                    tyi = r / f.X0n;
+                    txi = r - tyi * f.X0n;
+                    if (++k_in == kClaim) {
+                        base = next;
+                        k_in = 0;
+                        if (base < f.n0) next = atomicAdd(f.ctr, kClaim);
+                    }
+                } else {  // both queues drained
                     if (i >= NS) wait_empty(s, (use - 1) & 1);
                     task_sm[s] = make_int4(-1, 0, 0, 0);
                     mbar_arrive(&full[s]);  // consumers see the sentinel and stop
@@ -619,17 +648,12 @@ __global__ void __launch_bounds__((NW + 1) * 32,
                     flush();
                     break;
                 }
-                // consecutive task in the same tile row: next column
-                if (t == prev + 1 && t < row_end) ++txi;
-                else fused_decode(K.fu, t, lvl, b, tyi, txi, row_end);
-                prev = t;
                 const FastArgs& a = K.lv[lvl];
                 const int cx = a.X0 + (txi + a.tx0) * a.TW - HX;
                 const int cy = a.Y0 + (tyi + a.ty0) * a.TH - H - 1;
-                if (lvl == 1) fused_wait_rows(K, b, cy, G::kRows, known, idle);
                 if (i >= NS) wait_empty(s, (use - 1) & 1);
                 report(i - kRing + 1, true);  // ring slot i % kRing is free
-                row_ring[i & (kRing - 1)] = lvl == 0 ? b * K.fu.R0 + tyi : -1;
+                row_ring[i & (kRing - 1)] = lvl == 0 ? b * f.R0 + tyi : -1;
                 issued = i + 1;
                 task_sm[s] = make_int4(lvl, b, tyi, txi);
                 float* dst = stage + s * G::kStageFloats;
@@ -639,15 +663,7 @@ __global__ void __launch_bounds__((NW + 1) * 32,
                 for (int q = 0; q < WL_FWD_SPLIT; ++q)
                     tma_load_3d(dst + q * kSplitRows * 2 * TWC, lvl ? &m1 : &m0, &full[s], 2 * cx,
                                 2 * cy + q * kSplitRows, b);
-                if (++k_in == kClaim) {
-                    base = next;
-                    k_in = 0;
-#ifdef WL_FUSE_STATIC
-                    next = base + gridDim.x * kClaim;
-#else
-                    if (base < K.fu.ntasks) next = atomicAdd(K.fu.ctr, kClaim);
-#endif
-                }
+                if (p1 < f.n1) prefetch();
             }
         } else if (lane == 0) {
             bool halo_ready = false;
@@ -1503,28 +1519,8 @@ cudaError_t launch(const WlLevel& L, const Plan& plan, cudaStream_t stream) {
 }
 
 // Fused launch of two consecutive periodic forward levels (L1 reads L0's LL
-// output). `ctr` = fused_ctr_elems(...) zeroed words on the stream (memset
-// here). Returns cudaErrorNotSupported when the pair does not qualify.
-inline int fused_ready_c(const Plan& p0, const Plan& p1, int H, int kRows) {
-    // smallest c with ready(k) = min(2k+1+c, R0-1) >= the last level-l tile
-    // row every level-(l+1) tile row k >= 1 reads (k = 0 wraps: last anyway)
-    const FastArgs& a0 = p0.args;
-    const FastArgs& a1 = p1.args;
-    const int R0 = p0.tiles_y, R1 = p1.tiles_y, qh0 = a0.qh;
-    auto fdiv = [](int x, int y) { return x >= 0 ? x / y : -((-x + y - 1) / y); };
-    int c = 0;
-    for (int k = 1; k < R1; ++k) {
-        const int cy = a1.Y0 + (k + a1.ty0) * a1.TH - H - 1;
-        const int ya = 2 * cy, yb = 2 * (cy + kRows);
-        int need;
-        if (ya < 0 || yb > qh0) need = R0 - 1;  // wraps: needs the last row
-        else need = fdiv(yb - 1 - a0.Y0, a0.TH) - a0.ty0;
-        if (need > R0 - 1) need = R0 - 1;
-        while (std::min(2 * k + 1 + c, R0 - 1) < need) ++c;
-    }
-    return c;
-}
-
+// output). `ctr` = wl_fused_ctr_elems(...) words (zeroed here, on the stream).
+// Returns cudaErrorNotSupported when the pair does not qualify.
 template <class P, int DIR, int R, int NW, int CPT, int NS, bool XF, int MAXB>
 cudaError_t launch_fused(const WlLevel& L0, const Plan& p0, const WlLevel& L1, const Plan& p1,
                          unsigned* ctr, cudaStream_t stream) {
@@ -1549,36 +1545,17 @@ cudaError_t launch_fused(const WlLevel& L0, const Plan& p0, const WlLevel& L1, c
         f.R1 = p1.tiles_y;
         f.X0n = p0.args.tiles_x;
         f.X1n = p1.args.tiles_x;
-        f.c = fused_ready_c(p0, p1, P::kHalo, G::kRows);
-        const long per_img = (long)f.R0 * f.X0n + (long)f.R1 * f.X1n;
-        if ((long)nb * per_img >= (1l << 30) || (long)nb * f.R0 >= (1l << 30))
+        if ((long)nb * f.R0 * f.X0n >= (1l << 30) || (long)nb * f.R1 * f.X1n >= (1l << 30))
             return cudaErrorNotSupported;
-        f.ntasks = (int)(nb * per_img);
-        static const int diag = [] {  // timing diagnostic: 1 = level-l tiles only
-            const char* v = getenv("WL_FUSE_DIAG");
-            return v ? atoi(v) : 0;
-        }();
-        if (diag == 1) {
-            f.R1 = 0;
-            f.ntasks = nb * f.R0 * f.X0n;
-        }
+        f.n0 = nb * f.R0 * f.X0n;
+        f.n1 = nb * f.R1 * f.X1n;
         f.target = (unsigned)f.X0n * NW;
         static int cap[64] = {};
         auto kern = fast_kernel<P, DIR, R, NW, CPT, NS, XF, false, true>;
         const int mb = grid_cap<R, NW, CPT, NS, NXC, MAXB>(kern, cap);
-        const int grid = f.ntasks < mb ? f.ntasks : mb;
-        // lag: the tasks claimed but possibly unfinished (grid x stages), in
-        // level-l rows of the sequence (X0n + X1n/2 tasks each), plus one
-        {
-            static const int dmul = [] {
-                const char* v = getenv("WL_FUSE_LAG");
-                return v ? atoi(v) : 150;
-            }();
-            const int per_row = f.X0n + (f.X1n + 1) / 2;
-            const long inflight = (long)grid * (NS + 2 * WL_FUSE_CLAIM);
-            f.D = (int)((inflight * dmul / 100 + per_row - 1) / per_row) + 1;
-        }
-        cudaError_t e = cudaMemsetAsync(ctr, 0, (1 + (size_t)nb * f.R0) * sizeof(unsigned), stream);
+        const int ntasks = f.n0 + f.n1;
+        const int grid = ntasks < mb ? ntasks : mb;
+        cudaError_t e = cudaMemsetAsync(ctr, 0, (2 + (size_t)nb * f.R0) * sizeof(unsigned), stream);
         if (e != cudaSuccess) return e;
         // maps: m0 = level-l image, m1 = level-(l+1) input (= LL_l)
         cudaError_t le = launch_pdl(kern, dim3(grid), dim3((NW + 1) * 32), G::kSmemBytes, stream,
