@@ -246,8 +246,8 @@ __device__ __forceinline__ unsigned ld_acquire_sys_u32(const unsigned* p) {
     asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
-__device__ inline void wait_halo_flags(const unsigned* fa, const unsigned* fb, unsigned e,
-                                       unsigned* err) {
+static __device__ __noinline__ void wait_halo_flags(const unsigned* fa, const unsigned* fb, unsigned e,
+                                             unsigned* err) {
     unsigned long long t0, t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
     unsigned ns = 64;
@@ -688,9 +688,8 @@ __global__ void __launch_bounds__((NW + 1) * 32,
 #endif
                 }
                 const int b = t / a.ntiles_img, tt = t - b * a.ntiles_img;
-                const int ntr = a.ntiles_img / a.tiles_x;
                 const int tyk = tt / a.tiles_x;
-                const int tyi = tile_row_of(tyk, ntr, a.xflag_a != nullptr);
+                const int tyi = a.xflag_a ? tile_row_of(tyk, a.ntiles_img / a.tiles_x, true) : tyk;
                 const int ty = tyi + a.ty0, tx = tt - tyk * a.tiles_x + a.tx0;
                 const int cx = a.X0 + tx * a.TW - HX;     // first compute cell column
                 const int cy = a.Y0 + ty * a.TH - H - 1;  // ghost row above the region
@@ -744,7 +743,7 @@ __global__ void __launch_bounds__((NW + 1) * 32,
             b = t / a0.ntiles_img;
             const int tt = t - b * a0.ntiles_img;
             const int tyk = tt / a0.tiles_x;
-            tyi = tile_row_of(tyk, a0.ntiles_img / a0.tiles_x, a0.xflag_a != nullptr);
+            tyi = a0.xflag_a ? tile_row_of(tyk, a0.ntiles_img / a0.tiles_x, true) : tyk;
             txi = tt - tyk * a0.tiles_x;
         }
         // The tile body, instantiated per level with compile-time offsets into
