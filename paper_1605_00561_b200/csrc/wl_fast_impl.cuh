@@ -43,20 +43,20 @@
 
 namespace wlfast {
 
-// Producer wait on a released stage: 0 = test_wait + __nanosleep back-off
-// (cap WL_PROD_BACKOFF_NS), 1 = try_wait with a suspend hint, 2 = plain
-// try_wait loop (hardware-timed suspend).
+// Producer wait on a released stage: test_wait + __nanosleep back-off (cap
+// per program, ProdBackoff). try_wait with a suspend hint or a plain try_wait
+// loop measured 10-40% slower (their polling competes with the compute warps).
 // Tuning knobs: pad the exchange buffer to at least this many component rows
 // (shared-memory footprint / residency experiments) and cap CTAs per SM
 // (0 = as many as fit).
 #ifndef WL_XCH_MIN
 #define WL_XCH_MIN 0
 #endif
-#ifndef WL_PROD_SLEEP
-#define WL_PROD_SLEEP 0
+#ifndef WL_PROD_EARLY
+#define WL_PROD_EARLY 0
 #endif
-#ifndef WL_PROD_HINT_NS
-#define WL_PROD_HINT_NS 1000000u
+#ifndef WL_PROD_BACKOFF97_NS
+#define WL_PROD_BACKOFF97_NS 1024
 #endif
 #ifndef WL_PROD_BACKOFF_NS
 #define WL_PROD_BACKOFF_NS 256
@@ -134,23 +134,13 @@ __device__ __forceinline__ bool mbar_test(uint64_t* b, unsigned parity) {
         : "memory");
     return ok != 0;
 }
+template <int CAP = WL_PROD_BACKOFF_NS>
 __device__ __forceinline__ void mbar_wait_backoff(uint64_t* b, unsigned parity) {
     unsigned ns = 32;
     while (!mbar_test(b, parity)) {
         __nanosleep(ns);
-        ns = ns < WL_PROD_BACKOFF_NS ? 2 * ns : WL_PROD_BACKOFF_NS;
+        ns = ns < CAP ? 2 * ns : CAP;
     }
-}
-// Producer wait, variant: try_wait with a suspend-time hint parks the thread
-// in hardware until the phase completes (no polling instructions).
-__device__ __forceinline__ void mbar_wait_sleep(uint64_t* b, unsigned parity) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n"
-        "WL_WAIT_S:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
-        "@!p bra WL_WAIT_S;\n}" ::"r"(smem_u32(b)),
-        "r"(parity), "r"(WL_PROD_HINT_NS)
-        : "memory");
 }
 // Fused pyramid launches: tasks claimed per atomic.
 #ifndef WL_FUSE_CLAIM
@@ -368,6 +358,24 @@ __device__ inline int fused_dep_rows(const KArgs& K, int cy, int rows, int (&j)[
     }
     return n;
 }
+
+// Producer back-off cap (ns) per program: the polling producer shares an SM
+// sub-partition with compute warps, so how long it sleeps between polls is
+// a trade-off between refill latency and stolen issue slots. Measured on
+// B200 at 16384^2 (profiles/tuning_r01_backoff.txt): 1024 ns for the cdf97
+// lifting inverses (+6-13%; two CTAs of 4 compute warps per SM share the
+// sub-partitions with the producers), 256 ns elsewhere (cdf53 inverses and
+// the FP32-heavy cdf97 Polyphase inverse lose with the longer cap; the
+// forwards are neutral within noise).
+template <class P, int DIR>
+struct ProdBackoff {
+    static constexpr int ns =
+        P::kHalo == 2 && DIR == 1 ? WL_PROD_BACKOFF97_NS : WL_PROD_BACKOFF_NS;
+};
+template <>
+struct ProdBackoff<P_cdf97_polyphase_inv, 1> {
+    static constexpr int ns = WL_PROD_BACKOFF_NS;
+};
 
 template <int R, int NW, int CPT, int NS = 2, int NXC = 4>
 struct Geometry {
@@ -678,15 +686,9 @@ __global__ void __launch_bounds__((NW + 1) * 32,
                 }
                 const int s = i % NS;
                 const unsigned use = i / NS;  // how often stage s was filled before
-                if (i >= NS) {
-#if WL_PROD_SLEEP == 1
-                    mbar_wait_sleep(&empty[s], (use - 1) & 1);
-#elif WL_PROD_SLEEP == 2
-                    mbar_wait(&empty[s], (use - 1) & 1);
-#else
-                    mbar_wait_backoff(&empty[s], (use - 1) & 1);
+#if !WL_PROD_EARLY
+                if (i >= NS) mbar_wait_backoff<ProdBackoff<P, DIR>::ns>(&empty[s], (use - 1) & 1);
 #endif
-                }
                 const int b = t / a.ntiles_img, tt = t - b * a.ntiles_img;
                 const int tyk = tt / a.tiles_x;
                 const int tyi = a.xflag_a ? tile_row_of(tyk, a.ntiles_img / a.tiles_x, true) : tyk;
@@ -697,6 +699,9 @@ __global__ void __launch_bounds__((NW + 1) * 32,
                     wait_halo_flags(a.xflag_a, a.xflag_b, a.xepoch, a.xerr);
                     halo_ready = true;
                 }
+#if WL_PROD_EARLY  // tile coordinates first: their divisions overlap the stage wait
+                if (i >= NS) mbar_wait_backoff<ProdBackoff<P, DIR>::ns>(&empty[s], (use - 1) & 1);
+#endif
                 float* dst = stage + s * G::kStageFloats;
                 mbar_expect_tx(&full[s], G::kStageBytes);
                 if (DIR == 0) {
