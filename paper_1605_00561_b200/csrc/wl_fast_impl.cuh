@@ -1210,7 +1210,7 @@ struct Config;
 #endif
 // exchange mode (1 = full) and CTAs-per-SM cap (0 = none) per configuration
 #ifndef WL_XF53F
-#define WL_XF53F 1
+#define WL_XF53F 0
 #endif
 #ifndef WL_XF53I
 #define WL_XF53I 0
@@ -1322,6 +1322,17 @@ struct SchemeConfig<1, 0, 7> : Config<1, 0> {
     static constexpr int R = WL_POLY_R;  // 30-row tiles x 10 warps (profiles/tuning_r01_poly.txt)
     static constexpr int NW = WL_POLY_NW;
 };
+
+// Tuning knob: one extra per-scheme override from the compiler command line
+// (-DWL_OVR_W=w -DWL_OVR_D=d -DWL_OVR_S=s -DWL_OVR_R=.. -DWL_OVR_NW=.. -DWL_OVR_NS=..
+// -DWL_OVR_XF=..), for A/B builds.
+#ifdef WL_OVR_S
+template <>
+struct SchemeConfig<WL_OVR_W, WL_OVR_D, WL_OVR_S> : Config<WL_OVR_W, WL_OVR_D> {
+    static constexpr int R = WL_OVR_R, NW = WL_OVR_NW, NS = WL_OVR_NS;
+    static constexpr bool XF = WL_OVR_XF;
+};
+#endif
 
 // cdf97 Monolithic / Monolithic* inverses: full exchange measured faster
 // (profiles/tuning_r01_exchange.txt).
