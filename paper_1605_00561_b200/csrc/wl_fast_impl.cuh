@@ -55,6 +55,9 @@ namespace wlfast {
 #ifndef WL_PROD_EARLY
 #define WL_PROD_EARLY 0
 #endif
+#ifndef WL_PROD_BO97_FWD  // the cdf97 forwards on the long cap too (A/B knob)
+#define WL_PROD_BO97_FWD 0
+#endif
 #ifndef WL_PROD_BACKOFF97_NS
 #define WL_PROD_BACKOFF97_NS 1024
 #endif
@@ -364,8 +367,9 @@ __device__ inline int fused_dep_rows(const KArgs& K, int cy, int rows, int (&j)[
 // forwards are neutral within noise).
 template <class P, int DIR>
 struct ProdBackoff {
-    static constexpr int ns =
-        P::kHalo == 2 && DIR == 1 ? WL_PROD_BACKOFF97_NS : WL_PROD_BACKOFF_NS;
+    static constexpr int ns = P::kHalo == 2 && (DIR == 1 || WL_PROD_BO97_FWD)
+                                  ? WL_PROD_BACKOFF97_NS
+                                  : WL_PROD_BACKOFF_NS;
 };
 template <>
 struct ProdBackoff<P_cdf97_polyphase_inv, 1> {
