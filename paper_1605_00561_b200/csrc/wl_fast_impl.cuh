@@ -1300,12 +1300,18 @@ struct SchemeConfig : Config<WAVELET, DIR> {};
 #ifndef WL_POLY_R
 #define WL_POLY_R 3
 #endif
+#ifndef WL_POLY_NS_FWD
+#define WL_POLY_NS_FWD 2
+#endif
+#ifndef WL_POLY_NS_INV
+#define WL_POLY_NS_INV 2
+#endif
 #ifndef WL_POLY_NW
 #define WL_POLY_NW 10
 #endif
 template <int SCHEME>
 struct PolyInv {
-    static constexpr int R = WL_POLY_R, NW = WL_POLY_NW, CPT = 4, NS = 2;
+    static constexpr int R = WL_POLY_R, NW = WL_POLY_NW, CPT = 4, NS = WL_POLY_NS_INV;
     static constexpr bool XF = false;
     static constexpr int MAXB = 0;
 };
@@ -1317,7 +1323,7 @@ struct SchemeConfig<1, 1, 7> : PolyInv<7> {};  // cdf97 polyphase inverse
 // (profiles/tuning_r01_tiles97.txt).
 template <>
 struct SchemeConfig<1, 0, 7> : Config<1, 0> {
-    static constexpr int NS = 2;
+    static constexpr int NS = WL_POLY_NS_FWD;
     static constexpr int R = WL_POLY_R;  // 30-row tiles x 10 warps (profiles/tuning_r01_poly.txt)
     static constexpr int NW = WL_POLY_NW;
 };
