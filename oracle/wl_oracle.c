@@ -1,8 +1,11 @@
 /*
  * TEST INFRASTRUCTURE -- CPU oracle, NOT the product.
  *
- * Plain-C restatement of the reference hot path (float64, single thread):
- * /root/reference/proj/src/transform.cpp. Only tests/, __graft_entry__.smoke()
+ * Plain-C restatement of the reference hot path (float64):
+ * /root/reference/proj/src/transform.cpp. Rows of a step are split over
+ * OpenMP threads (like parallel_rows, transform.cpp:36-55); every output
+ * element is computed by one thread in the reference's order, so the result
+ * is independent of the thread count (OMP_NUM_THREADS). Only tests/, __graft_entry__.smoke()
  * and bench.py's cpu_baseline leg may load this library, and only as the
  * checker. It is pinned against the unmodified reference (oracle/_ref) and
  * against the golden fixtures in tests/golden/ (see tests/test_oracle.py).
@@ -22,6 +25,14 @@ enum { LL = 0, HL = 1, LH = 2, HH = 3 };
 
 /* transform.cpp:59-72 resolve_index: periodic wrap or whole-point mirror
  * (iterated), n == 1 absorbs every index. */
+/* Worker threads of the parallel row loops (1 without OpenMP). */
+#ifdef _OPENMP
+#include <omp.h>
+int wlo_threads(void) { return omp_get_max_threads(); }
+#else
+int wlo_threads(void) { return 1; }
+#endif
+
 int wlo_resolve_index(int i, int n, int boundary) {
     if (i >= 0 && i < n) return i;
     if (n == 1) return 0;
@@ -75,6 +86,7 @@ void wlo_apply_step(const double* in4, int qw, int qh, const int* taps, const do
         while (t0 < ntaps && taps[5 * t0] != comp) ++t0;
         t1 = t0;
         while (t1 < ntaps && taps[5 * t1] == comp) ++t1;
+#pragma omp parallel for schedule(static)
         for (int r = 0; r < qh; ++r)
             for (int c = 0; c < qw; ++c) {
                 double acc = 0.0;
@@ -153,6 +165,7 @@ int wlo_forward_conv(const double* img, int w, int h, const int* ntap, const int
     static const int col_phase[4] = {0, 1, 0, 1};
     int off = 0;
     for (int comp = 0; comp < 4; ++comp) {
+#pragma omp parallel for schedule(static)
         for (int r = 0; r < qh; ++r)
             for (int c = 0; c < qw; ++c) {
                 double acc = 0.0;

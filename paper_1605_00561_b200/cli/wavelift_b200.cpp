@@ -32,6 +32,9 @@ struct Args {
     std::string size = "1024x1024", format = "text";
     int levels = 1, reps = 5;
     bool scaling = false, pad = false;
+    // opt-in extensions (off: the reference's exact behaviour and output)
+    bool scheme_inverse = false;  // roundtrip: the scheme's own inverse kernel
+    bool gpix = false;            // bench: add GPix/s to the output
 };
 
 int to_int(const std::string& s, const char* what) {
@@ -61,6 +64,8 @@ Args parse(int argc, char** argv, int first) {
         else if (k == "--format") a.format = val();
         else if (k == "--scaling") a.scaling = true;
         else if (k == "--pad") a.pad = true;
+        else if (k == "--scheme-inverse") a.scheme_inverse = true;
+        else if (k == "--gpix") a.gpix = true;
         else if (!k.empty() && k[0] == '-') throw std::invalid_argument("unknown option " + k);
         else a.pos.push_back(k);
     }
@@ -142,7 +147,10 @@ int cmd_roundtrip(const Args& a) {
                      "exact for --scheme sweldens or --boundary periodic\n",
                      scheme_name(kind).c_str());
     const Pyramid p = multi_level_forward(img, build_scheme(kind, w), a.levels, b, false);
-    const Image rec = multi_level_inverse(p, w, b, false, kind);
+    // The reference always inverts with the wavelet-only (Sweldens) inverse
+    // (wavelift_main.cpp:196); --scheme-inverse runs the scheme's own kernel.
+    const Image rec = a.scheme_inverse ? multi_level_inverse(p, w, b, false, kind)
+                                       : multi_level_inverse(p, w, b, false);
     double err = 0.0;
     for (std::size_t i = 0; i < img.samples.size(); ++i)
         err = std::max(err, std::abs(img.samples[i] - rec.samples[i]));
@@ -206,14 +214,20 @@ int cmd_bench(const Args& a) {
     const std::size_t m = seconds.size();
     const double med = (seconds[(m - 1) / 2] + seconds[m / 2]) / 2.0;
     const double mbps = static_cast<double>(bw) * bh * 8.0 / med / 1e6;  // the reference's unit
-    if (a.format == "csv")
+    const double gpix = static_cast<double>(bw) * bh / med / 1e9;
+    // wavelift_main.cpp:264-269 output; --gpix appends the GPixel/s figure
+    if (a.format == "csv" && a.gpix)
         std::printf("scheme,wavelet,size,mbps,gpix_s\n%s,%s,%dx%d,%.2f,%.2f\n",
-                    scheme_name(kind).c_str(), w.name.c_str(), bw, bh, mbps,
-                    static_cast<double>(bw) * bh / med / 1e9);
-    else
+                    scheme_name(kind).c_str(), w.name.c_str(), bw, bh, mbps, gpix);
+    else if (a.format == "csv")
+        std::printf("scheme,wavelet,size,mbps\n%s,%s,%dx%d,%.2f\n", scheme_name(kind).c_str(),
+                    w.name.c_str(), bw, bh, mbps);
+    else if (a.gpix)
         std::printf("%s/%s %dx%d: median %.2f MB/s over %d rep(s) (%.1f GPix/s, B200 float32)\n",
-                    scheme_name(kind).c_str(), w.name.c_str(), bw, bh, mbps, a.reps,
-                    static_cast<double>(bw) * bh / med / 1e9);
+                    scheme_name(kind).c_str(), w.name.c_str(), bw, bh, mbps, a.reps, gpix);
+    else
+        std::printf("%s/%s %dx%d: median %.2f MB/s over %d rep(s)\n", scheme_name(kind).c_str(),
+                    w.name.c_str(), bw, bh, mbps, a.reps);
     return kExitOk;
 }
 
@@ -222,9 +236,9 @@ void usage() {
                  "usage: wavelift_b200 transform INPUT OUTPUT [--wavelet W] [--scheme S] "
                  "[--levels L] [--boundary B] [--scaling] [--pad]\n"
                  "       wavelift_b200 roundtrip INPUT [--wavelet W] [--scheme S] [--levels L] "
-                 "[--boundary B]\n"
+                 "[--boundary B] [--scheme-inverse]\n"
                  "       wavelift_b200 bench [--size WxH] [--wavelet W] [--scheme S] [--reps N] "
-                 "[--format text|csv]\n");
+                 "[--format text|csv] [--gpix]\n");
 }
 
 }  // namespace

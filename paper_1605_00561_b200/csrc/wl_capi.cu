@@ -2,6 +2,7 @@
 // reference's error semantics, engine dispatch, and the multi-level pyramid
 // driver (transform.cpp:198-256).
 #include <atomic>
+#include <cstdint>
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
@@ -339,6 +340,42 @@ int wl_forward_strip_wait(const float* strip, int w, int rows, int halo_rows, lo
     if (!wl_fast_supported(L))
         return fail(WL_EINVAL, "strip transform needs 16-byte aligned buffers and pitches");
     return cuda_status(wl_launch_fast(L, s), "fast_kernel");
+}
+
+bool wl_strip_shape_ok(int w, int rows, int halo_rows, int wavelet, int scheme, int direction) {
+    if (w <= 0 || rows <= 0 || !valid_ids(wavelet, scheme, 0) || wavelet > WL_CDF97) return false;
+    if (direction == 1 && scheme == WL_CONVOLUTION) scheme = WL_SWELDENS;
+    const WlProgram& P = wl_host_program(prog_index(wavelet, scheme, direction));
+    if (P.is_conv) return w % 2 == 0 && rows % 2 == 0;  // the conv kernel takes any even shape
+    // a level descriptor shaped like the strip call's, at dummy aligned addresses
+    const float* dummy = reinterpret_cast<const float*>(static_cast<uintptr_t>(1) << 20);
+    WlLevel L{};
+    L.wavelet = wavelet;
+    L.scheme = scheme;
+    L.direction = direction;
+    L.prog = prog_index(wavelet, scheme, direction);
+    L.boundary = WL_PERIODIC;
+    for (int k = 0; k < 4; ++k) {
+        L.in[k] = dummy;
+        L.out[k] = const_cast<float*>(dummy);
+    }
+    if (direction == 0) {
+        if (w % 2 || rows % 2 || halo_rows % 2) return false;
+        L.qw = w / 2;
+        L.qh = rows / 2 + halo_rows;
+        L.in_pitch = w;
+        L.out_pitch = w / 2;
+        L.ylo = halo_rows / 2;
+        L.yhi = L.ylo + rows / 2;
+    } else {
+        L.qw = w;
+        L.qh = rows + 2 * halo_rows;
+        L.in_pitch = w;
+        L.out_pitch = 2 * w;
+        L.ylo = halo_rows;
+        L.yhi = halo_rows + rows;
+    }
+    return wl_fast_supported(L);
 }
 
 extern "C" {

@@ -64,19 +64,30 @@ struct Workspace {
             }
         }
         if (in_floats > in_cap || out_floats > out_cap) {
-            for (int s = 0; s < kMaxSlots; ++s) {
-                cudaFree(in[s]);
-                cudaFree(out[s]);
-                in[s] = out[s] = nullptr;
-            }
-            in_cap = in_floats > in_cap ? in_floats : in_cap;
-            out_cap = out_floats > out_cap ? out_floats : out_cap;
+            free_buffers();
+            const size_t ni = in_floats > in_cap ? in_floats : in_cap;
+            const size_t no = out_floats > out_cap ? out_floats : out_cap;
+            in_cap = out_cap = 0;
             for (int s = 0; s < slots(); ++s) {
-                if (cudaMalloc(&in[s], in_cap * sizeof(float)) != cudaSuccess) return false;
-                if (cudaMalloc(&out[s], out_cap * sizeof(float)) != cudaSuccess) return false;
+                if (cudaMalloc(&in[s], ni * sizeof(float)) != cudaSuccess ||
+                    cudaMalloc(&out[s], no * sizeof(float)) != cudaSuccess) {
+                    // no half-allocated slots: the next call retries from scratch
+                    free_buffers();
+                    cudaGetLastError();
+                    return false;
+                }
             }
+            in_cap = ni;  // only once every slot holds its buffers
+            out_cap = no;
         }
         return true;
+    }
+    void free_buffers() {
+        for (int s = 0; s < kMaxSlots; ++s) {
+            cudaFree(in[s]);
+            cudaFree(out[s]);
+            in[s] = out[s] = nullptr;
+        }
     }
     void release() {
         if (device < 0) return;
@@ -99,6 +110,14 @@ struct Workspace {
 thread_local Workspace g_ws;
 
 int herr(int code, const std::string& m) { return wl_fail(code, m.c_str()); }
+
+// A failed chunk pipeline must not return while copies of earlier chunks
+// still read or write the caller's (pinned) host buffers.
+int drain(int code) {
+    for (int k = 0; k < 3; ++k)
+        if (g_ws.streams[k]) cudaStreamSynchronize(g_ws.streams[k]);
+    return code;
+}
 
 int cuda_err(cudaError_t e, const char* where) {
     return herr(WL_ERUNTIME, std::string(where) + ": " + cudaGetErrorString(e));
@@ -218,9 +237,13 @@ int wl_dwt2_forward_host(const float* img, int w, int h, long img_pitch, int wav
     float* hp[4] = {ll, hl, lh, hh};
     const int halo = (wavelet == WL_CDF53 || wavelet == WL_CDF97)
                          ? wl_strip_halo_rows(wavelet, scheme, 0) : -1;
-    const bool chunked = boundary == WL_PERIODIC && halo > 0 && (w % 4) == 0 && h >= 2 * halo &&
-                         scheme >= 0 && scheme <= 9;
+    bool chunked = boundary == WL_PERIODIC && halo > 0 && h >= 2 * halo && scheme >= 0 &&
+                   scheme <= 9;
     const int R = chunked ? chunk_rows(4L * w, h, 2) : h;
+    // every chunk height of the plan must be a shape the strip kernels take
+    if (chunked && R < h)
+        for (int rows : chunk_plan(h, R, 2))
+            chunked = chunked && wl_strip_shape_ok(w, rows, halo, wavelet, scheme, 0);
     if (!chunked || R >= h) {
         // whole image: one slot, copy in / transform / copy out
         const size_t nin = static_cast<size_t>(w) * h, nout = 4 * static_cast<size_t>(qw) * (h / 2);
@@ -234,11 +257,11 @@ int wl_dwt2_forward_host(const float* img, int w, int h, long img_pitch, int wav
         float* o = g_ws.out[0];
         int st = wl_dwt2_forward(d, w, h, w, wavelet, scheme, boundary, scaling, o, o + np,
                                  o + 2 * np, o + 3 * np, qw, s);
-        if (st != WL_OK) return st;
+        if (st != WL_OK) return drain(st);
         for (int c = 0; c < 4; ++c) {
             e = cudaMemcpy2DAsync(hp[c], plane_pitch * 4, o + c * np, qw * 4, qw * 4, h / 2,
                                   cudaMemcpyDeviceToHost, s);
-            if (e != cudaSuccess) return cuda_err(e, "D2H");
+            if (e != cudaSuccess) return drain(cuda_err(e, "D2H"));
         }
         e = cudaStreamSynchronize(s);
         return e == cudaSuccess ? WL_OK : cuda_err(e, "forward_host");
@@ -273,10 +296,10 @@ int wl_dwt2_forward_host(const float* img, int w, int h, long img_pitch, int wav
                 }
                 return cudaSuccess;
             });
-        if (r != WL_OK) return r;
+        if (r != WL_OK) return drain(r);
     }
     const cudaError_t e = cudaStreamSynchronize(g_ws.streams[2]);  // last D2H waits on all
-    return e == cudaSuccess ? WL_OK : cuda_err(e, "forward_host");
+    return e == cudaSuccess ? WL_OK : drain(cuda_err(e, "forward_host"));
 }
 
 int wl_dwt2_inverse_host(const float* ll, const float* hl, const float* lh, const float* hh,
@@ -288,9 +311,12 @@ int wl_dwt2_inverse_host(const float* ll, const float* hl, const float* lh, cons
     const float* hp[4] = {ll, hl, lh, hh};
     const int halo = (wavelet == WL_CDF53 || wavelet == WL_CDF97)
                          ? wl_strip_halo_rows(wavelet, scheme, 1) : -1;
-    const bool chunked = boundary == WL_PERIODIC && halo > 0 && (qw % 4) == 0 &&
-                         qh >= 2 * halo && scheme >= 0 && scheme <= 9;
+    bool chunked = boundary == WL_PERIODIC && halo > 0 && qh >= 2 * halo && scheme >= 0 &&
+                   scheme <= 9;
     const int R = chunked ? chunk_rows(16L * qw, qh, 1) : qh;
+    if (chunked && R < qh)
+        for (int rows : chunk_plan(qh, R, 1))
+            chunked = chunked && wl_strip_shape_ok(qw, rows, halo, wavelet, scheme, 1);
     if (!chunked || R >= qh) {
         const size_t np = static_cast<size_t>(qw) * qh;
         if (!g_ws.ensure(4 * np, 4 * np))
@@ -300,15 +326,15 @@ int wl_dwt2_inverse_host(const float* ll, const float* hl, const float* lh, cons
         for (int c = 0; c < 4; ++c) {
             cudaError_t e = cudaMemcpy2DAsync(d + c * np, qw * 4, hp[c], plane_pitch * 4, qw * 4,
                                               qh, cudaMemcpyHostToDevice, s);
-            if (e != cudaSuccess) return cuda_err(e, "H2D");
+            if (e != cudaSuccess) return drain(cuda_err(e, "H2D"));
         }
         float* o = g_ws.out[0];
         int st = wl_dwt2_inverse(d, d + np, d + 2 * np, d + 3 * np, qw, qh, qw, wavelet, scheme,
                                  boundary, undo_scaling, o, 2 * qw, s);
-        if (st != WL_OK) return st;
+        if (st != WL_OK) return drain(st);
         cudaError_t e = cudaMemcpy2DAsync(img, img_pitch * 4, o, 2 * qw * 4, 2 * qw * 4, 2 * qh,
                                           cudaMemcpyDeviceToHost, s);
-        if (e != cudaSuccess) return cuda_err(e, "D2H");
+        if (e != cudaSuccess) return drain(cuda_err(e, "D2H"));
         e = cudaStreamSynchronize(s);
         return e == cudaSuccess ? WL_OK : cuda_err(e, "inverse_host");
     }
@@ -343,10 +369,10 @@ int wl_dwt2_inverse_host(const float* ll, const float* hl, const float* lh, cons
                                  g_ws.out[s], 2 * qw, 2 * qw, 2 * rows, cudaMemcpyDeviceToHost,
                                  st);
             });
-        if (r != WL_OK) return r;
+        if (r != WL_OK) return drain(r);
     }
     const cudaError_t e = cudaStreamSynchronize(g_ws.streams[2]);  // last D2H waits on all
-    return e == cudaSuccess ? WL_OK : cuda_err(e, "inverse_host");
+    return e == cudaSuccess ? WL_OK : drain(cuda_err(e, "inverse_host"));
 }
 
 }  // extern "C"

@@ -76,3 +76,9 @@ int wl_forward_strip_wait(const float* strip, int w, int rows, int halo_rows, lo
                           int wavelet, int scheme, int scaling, float* ll, float* hl, float* lh,
                           float* hh, long plane_pitch, void* stream, const unsigned* xflag_a,
                           const unsigned* xflag_b, unsigned xepoch, unsigned* xerr);
+
+// Can the strip transforms run this shape on dense buffers (pitch = width)
+// at 256-byte aligned addresses? forward: w pixels x rows (+ halo_rows above
+// and below); inverse (direction 1): w = plane cells, rows = plane rows.
+// Asked by the host chunk pipeline and WlStrips BEFORE anything is enqueued.
+bool wl_strip_shape_ok(int w, int rows, int halo_rows, int wavelet, int scheme, int direction);

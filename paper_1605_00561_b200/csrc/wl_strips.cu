@@ -197,6 +197,12 @@ int wl_strips_create(int w, int h, int rank, int nranks, int levels, int wavelet
         return sfail(WL_EINVAL, "strip too thin for the halo at the deepest level");
     if (((w >> (levels - 1)) * 4) % 16 != 0)
         return sfail(WL_EINVAL, "level widths must keep 16-byte aligned rows");
+    // every level's strip transform must accept its shape: checked here, before
+    // any exchange kernel or flag signal of a forward call is enqueued
+    for (int l = 0; l < levels; ++l)
+        if (!wl_strip_shape_ok(w >> l, rows >> l, halo, wavelet, scheme, 0))
+            return sfail(WL_EINVAL, "a pyramid level's width is not supported by the strip "
+                                    "kernels (lifting schemes need level widths = 0 mod 8)");
     WlStrips* s = new (std::nothrow) WlStrips();
     if (!s) return sfail(WL_ERUNTIME, "out of host memory");
     s->w = w;

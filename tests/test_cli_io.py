@@ -105,6 +105,20 @@ def test_cli_roundtrip_and_bench(tmp_path):
     for w in ("cdf53", "cdf97"):
         r = run_cli("roundtrip", pgm, "--wavelet", w, "--scheme", "monolithic_star", "--levels", 3)
         assert r.returncode == 0 and "OK" in r.stdout, r.stdout + r.stderr
+    # wavelift_main.cpp:196: the reference inverts with the wavelet-only
+    # (Sweldens) inverse, so a symmetric non-Sweldens roundtrip FAILs (exit 2)
+    # there; --scheme-inverse runs the scheme's own inverse kernel instead.
+    r = run_cli("roundtrip", pgm, "--scheme", "monolithic", "--boundary", "symmetric")
+    assert r.returncode == 2 and "FAIL" in r.stdout and "note:" in r.stderr, r.stdout
+    r = run_cli("roundtrip", pgm, "--scheme", "monolithic", "--boundary", "symmetric",
+                "--scheme-inverse")
+    assert r.returncode == 0 and "OK" in r.stdout, r.stdout + r.stderr
     r = run_cli("bench", "--size", "2048x1024", "--wavelet", "cdf97", "--scheme",
                 "monolithic_star", "--reps", 3, "--format", "csv")
-    assert r.returncode == 0 and r.stdout.startswith("scheme,wavelet,size,mbps"), r.stderr
+    lines = r.stdout.splitlines()
+    assert r.returncode == 0 and lines[0] == "scheme,wavelet,size,mbps", r.stderr
+    assert lines[1].startswith("monolithic_star,cdf97,2048x1024,") and lines[1].count(",") == 3
+    r = run_cli("bench", "--size", "256x256", "--reps", 2)
+    assert r.returncode == 0 and r.stdout.rstrip().endswith("over 2 rep(s)"), r.stdout
+    r = run_cli("bench", "--size", "256x256", "--reps", 2, "--format", "csv", "--gpix")
+    assert r.stdout.splitlines()[0] == "scheme,wavelet,size,mbps,gpix_s", r.stdout
