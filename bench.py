@@ -10,18 +10,29 @@ reference's cmd_bench, wavelift_main.cpp:236-272). 40 passes of 67.1 MPix.
              (inputs resident in HBM; inputs > L2, so no flush needed).
 * e2e        same metric through the public API with HOST (pinned) buffers:
              each pass copies its input H2D and its result D2H inside the
-             timed region.
+             timed region; pcie = the box's plain pinned-copy ceiling.
+* per_scheme [ms, GPix/s, fraction of the HBM copy peak] per program, each
+             program timed ISOLATED: back-to-back launches of that program
+             alone (warm), median of the CUDA-event launch times.
 * roofline   dominant kernel of the step (largest share of step time):
              algorithmic bytes = 8 B/pixel (one f32 read + one f32 write per
-             pixel) / its CUDA-event launch time, against the
-             measured HBM copy peak (MEASURED_PEAKS.json).
-* c3         BASELINE.json configs[2]: cdf97 monolithic_star, 16384^2, fwd & inv.
-* per_scheme GPix/s, ns/px and HBM fraction for each of the 40 programs.
+             pixel) / its isolated median launch time, against
+             the measured HBM copy peak (MEASURED_PEAKS.json).
 * cpu_baseline  the unmodified reference (oracle/_ref, "reference") on the
-             host cores, bounded sample (see its "sample").
+             host cores at the FULL configs[1] size for the headline pair
+             (cdf53 Monolithic, cdf97 Monolithic*; forward + reference
+             inverse), with the GPU's isolated times of the same programs.
+* north_star (last key, so it survives a tail-truncated log)
+             c3 = configs[2] (16384^2: cdf97 Monolithic*, Monolithic,
+             Sweldens; cdf53 Monolithic, Monolithic*; fwd & inv, each with
+             its fraction of the copy peak and ncu DRAM traffic ratio),
+             c4 = configs[3] (32768^2 5-level strip pyramid),
+             c5 = configs[4] (4096 x 4096^2 3-level batches).
 
-`--impl reference` times the reference's CPU implementation of the same step
-on a bounded 512^2 sample (rank 0 only under torchrun).
+`--impl reference` times the reference's CPU implementation of the SAME step
+(same config object) on a bounded sample: every program forward + reference
+inverse on an 8192-wide band of --ref-rows rows per step (rank 0 only under
+torchrun).
 Multi-GPU (torchrun): every rank runs the full step on its own image(s)
 (independent images, no data-path collective; weak scaling); time = max over
 ranks of the device time.
@@ -149,6 +160,41 @@ def barrier(ws):
         dist.barrier()
 
 
+# ------------------------------------------------------------ shared config
+PROGRAMS = [(w, s) for w in WAVELETS for s in SCHEMES]
+# the reference CPU timed at the full configs[1] size (the headline pair)
+CPU_FULL = (("cdf53", "monolithic"), ("cdf97", "monolithic_star"))
+# configs[2] ablation at 16384^2: the north-star kernels and their neighbours
+C3_PROGRAMS = (("cdf97", "monolithic_star"), ("cdf97", "monolithic"), ("cdf97", "sweldens"),
+               ("cdf53", "monolithic"), ("cdf53", "monolithic_star"))
+
+
+def workload_config(n, ws):
+    """The step's config object -- identical in both arms (--impl b200 and
+    --impl reference), which time the same workload."""
+    return {"workload": f"configs[1]: every scheme x {{cdf53, cdf97}}, single-level forward + "
+                        f"that scheme's inverse, {n}x{n} float32 per rank, periodic, no scaling",
+            "size": n, "programs": len(PROGRAMS),
+            "pixels_per_step_per_rank": 2 * len(PROGRAMS) * n * n,
+            "l2": "inputs (256 MiB) larger than L2 (126 MB); no flush",
+            "parallelism": f"independent images, {ws} rank(s)"}
+
+
+def traffic_of(key):
+    """ncu DRAM bytes (read + write) per launch for `key`, from the newest
+    profiles/traffic_rNN.json (one `ncu --set full` capture per kernel)."""
+    for r in ("r02", "r01"):
+        path = os.path.join(ROOT, "profiles", f"traffic_{r}.json")
+        if os.path.exists(path):
+            try:
+                v = json.load(open(path)).get(key)
+            except Exception:
+                v = None
+            if v is not None:
+                return v
+    return None
+
+
 # --------------------------------------------------------------- reference arm
 def reference_step_sample(ref, img):
     """One bounded sample of the step on the reference CPU path: every scheme
@@ -163,21 +209,28 @@ def reference_step_sample(ref, img):
     return px
 
 
+def _ref_lib():
+    from oracle.oracle import Oracle, RefLib
+    try:
+        ref = RefLib()
+        return ref, "reference", ref.worker_count()
+    except FileNotFoundError:
+        o = Oracle()
+        return o, "port", int(o.lib.wlo_threads())
+
+
 def run_reference(args):
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     import numpy as np
-    from oracle.oracle import RefLib, Oracle
-    n = args.ref_size
-    try:
-        ref = RefLib()
-        kind = "reference"
-    except FileNotFoundError:
-        ref, kind = Oracle(), "port"
-    img = np.random.default_rng(12345).random((n, n))
-    cores = ref.worker_count() if kind == "reference" else 1
+    n, rows = args.size, args.ref_rows
+    ref, kind, cores = _ref_lib()
+    # a band of the configs[1] image: full 8192-pixel rows, --ref-rows rows
+    # (periodic), so every per-row cost is the full-size one; the whole
+    # --steps/--warmup run stays within a few minutes
+    img = np.random.default_rng(12345).random((rows, n))
     for _ in range(args.warmup):
         reference_step_sample(ref, img)
     times, px = [], 0
@@ -187,8 +240,9 @@ def run_reference(args):
         times.append(time.perf_counter() - t0)
     tot = sum(times)
     gpix = px * args.steps / tot / 1e9
-    sample = (f"{n}x{n} float64 uniform[0,1) (mt-free numpy seed 12345), every scheme x "
-              f"{{cdf53,cdf97}} forward + reference inverse per step, periodic, no scaling, "
+    sample = (f"per step: a {n}x{rows} band (full {n}-pixel rows) of the {n}x{n} configs[1] "
+              f"workload, float64 uniform[0,1) (numpy seed 12345); every scheme x {{cdf53,cdf97}} "
+              f"forward + the reference inverse; periodic, no scaling; "
               f"WAVELIFT_THREADS={os.environ.get('WAVELIFT_THREADS', 'unset')} -> {cores} "
               f"worker threads")
     line = {"impl": "reference", "metric": METRIC, "value": gpix, "unit": "GPixel/s",
@@ -196,8 +250,7 @@ def run_reference(args):
             "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "ns_per_pixel": 1e9 * tot / (px * args.steps),
-            "config": {"workload": f"configs[1] sample: {n}^2, all schemes x cdf53/cdf97, "
-                                   "fwd + inv", "size": n, "parallelism": "host threads"},
+            "config": workload_config(n, ws),
             "cpu_baseline": {"value": gpix, "unit": "GPixel/s", "cores": cores, "kind": kind,
                              "sample": sample},
             "e2e": {"value": gpix, "unit": "GPixel/s", "h2d_bytes_per_step": 0,
@@ -207,6 +260,34 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------- GPU arm
+def time_isolated(fn, stream, groups=5, per_group=10, warm=2):
+    """Steady-state device time (ms) of one call of fn: `groups` groups of
+    `per_group` back-to-back calls (no host sync in between), each group
+    between two CUDA events on the launching stream; median of the group
+    means (a single launch between two events is quantised to ~2 us)."""
+    import torch
+    for _ in range(warm):
+        fn()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(groups)]
+    for a, b in ev:
+        a.record(stream)
+        for _ in range(per_group):
+            fn()
+        b.record(stream)
+    torch.cuda.synchronize()
+    return statistics.median(a.elapsed_time(b) / per_group for a, b in ev)
+
+
+def prog_entry(t_ms, n, peak, traffic=None):
+    gbs = 8.0 * n * n / (t_ms * 1e-3) / 1e9
+    e = {"ms": round(t_ms, 5), "gpix_s": round(n * n / t_ms / 1e6, 1),
+         "hbm_gbs": round(gbs, 1), "frac": round(gbs / peak, 4)}
+    if traffic is not None:
+        e["traffic_ratio"] = round(traffic / (8.0 * n * n), 3)
+    return e
+
+
 def run_gpu(args):
     import torch
 
@@ -220,21 +301,13 @@ def run_gpu(args):
     img = torch.rand((n, n), device=dev, generator=g, dtype=torch.float32)
     rec = torch.empty_like(img)
     q = torch.empty((4, n // 2, n // 2), device=dev, dtype=torch.float32)
-    programs = [(w, s) for w in WAVELETS for s in SCHEMES]
-    schemes = {(w, s): wl.build_scheme(s, w) for (w, s) in programs}
+    schemes = {(w, s): wl.build_scheme(s, w) for (w, s) in PROGRAMS}
     stream = torch.cuda.current_stream()
 
-    def step(events=None):
-        for i, (w, s) in enumerate(programs):
-            if events is not None:
-                events[4 * i].record(stream)
+    def step():
+        for (w, s) in PROGRAMS:
             wl.forward(img, schemes[(w, s)], "periodic", False, out=q)
-            if events is not None:
-                events[4 * i + 1].record(stream)
-                events[4 * i + 2].record(stream)
             wl.inverse(q, w, "periodic", False, scheme=s, out=rec)
-            if events is not None:
-                events[4 * i + 3].record(stream)
 
     for _ in range(max(args.warmup, 3)):
         step()
@@ -254,29 +327,26 @@ def run_gpu(args):
         torch.cuda.synchronize()
         barrier(ws)
     launches = wl.launch_count() - n0
+    clocks = clk.summary()
     ms = start.elapsed_time(stop) / args.steps
     ms = barrier_max(ms, ws)
-    px_step = 2 * len(programs) * n * n
+    px_step = 2 * len(PROGRAMS) * n * n
     value = ws * px_step / (ms * 1e-3) / 1e9
 
-    # ---- per-kernel times (CUDA events on the launching stream), separate pass
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4 * len(programs))]
-    per = {}
-    reps = max(1, min(args.steps, 5))
-    acc = [0.0] * (2 * len(programs))
-    for _ in range(reps):
-        step(ev)
-        torch.cuda.synchronize()
-        for i in range(2 * len(programs)):
-            acc[i] += ev[2 * i].elapsed_time(ev[2 * i + 1])
-    algo_bytes = 8.0 * n * n
-    for i, (w, s) in enumerate(programs):
-        for d, name in ((0, "fwd"), (1, "inv")):
-            t = acc[2 * i + d] / reps
-            gbs = algo_bytes / (t * 1e-3) / 1e9
-            per[f"{w}/{s}/{name}"] = {"ms": round(t, 5), "gpix_s": round(n * n / t / 1e6, 2),
-                                      "ns_per_px": round(t * 1e6 / (n * n), 6),
-                                      "hbm_gbs": round(gbs, 1), "frac": round(gbs / peak, 4)}
+    # ---- per-program times: each program ISOLATED (back-to-back launches of
+    # that program alone, warm), median of the CUDA-event launch times
+    per, per_ms = {}, {}
+    for (w, s) in PROGRAMS:
+        sch = schemes[(w, s)]
+        tf = time_isolated(lambda: wl.forward(img, sch, "periodic", False, out=q), stream)
+        ti = time_isolated(lambda: wl.inverse(q, w, "periodic", False, scheme=s, out=rec),
+                           stream)
+        for d, t in (("fwd", tf), ("inv", ti)):
+            key = f"{w}/{s}/{d}"
+            per_ms[key] = t
+            e = prog_entry(t, n, peak)
+            per[key] = [e["ms"], e["gpix_s"], e["frac"]]
+
     # dominant kernel = largest share of the step, per actual kernel: the
     # Convolution scheme's inverse is the reference inverse (the Sweldens
     # inverse kernel), so both programs' launches count for that kernel
@@ -284,104 +354,59 @@ def run_gpu(args):
         w_, s_, d_ = prog.split("/")
         return f"{w_}/sweldens/inv" if (s_ == "convolution" and d_ == "inv") else prog
     share = {}
-    for k, v in per.items():
-        share[kernel_of(k)] = share.get(kernel_of(k), 0.0) + v["ms"]
+    for k, t in per_ms.items():
+        share[kernel_of(k)] = share.get(kernel_of(k), 0.0) + t
     dom = max(share, key=share.get)
-    dom_t = per[dom]["ms"]
-    step_sum = sum(v["ms"] for v in per.values())
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "traffic_r01.json")
-    if os.path.exists(tpath):
-        try:
-            traffic = json.load(open(tpath)).get(dom)
-        except Exception:
-            traffic = None
+    dom_t = per_ms[dom]
+    step_sum = sum(per_ms.values())
+    dom_e = prog_entry(dom_t, n, peak)
     # FP32 side of the same kernel: MACs per quad (count_macs, schemes.cpp:176)
-    # -> FMA per pixel = MACs / 4; nominal FP32 peak 148 SMs x 128 FMA/clk x
-    # 2 FLOP x max SM clock.
+    # -> FMA per pixel = MACs / 4; FP32 peak = SMs x 128 FMA/clk x 2 x SM clock.
     dw, ds, dd = dom.split("/")
     macs = schemes[(dw, ds)].info(0 if dd == "fwd" or ds == "convolution" else 1)["macs"]
-    fp32_peak = 148 * 128 * 2 * 1.965e9 / 1e12
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    clk_hz = (clocks.get("sm_max_mhz") or 1965.0) * 1e6
+    fp32_peak = sms * 128 * 2 * clk_hz / 1e12
     fp32 = 2.0 * macs / 4.0 * n * n / (dom_t * 1e-3) / 1e12
-    roofline = {"bound": "hbm", "kernel": dom, "achieved": per[dom]["hbm_gbs"], "peak": peak,
-                "peak_source": peak_src, "unit": "GB/s", "frac": per[dom]["frac"],
-                "traffic": traffic, "share_of_step": round(share[dom] / step_sum, 4),
-                "launches_per_step": sum(1 for k in per if kernel_of(k) == dom),
-                "algorithmic_bytes_per_launch": algo_bytes,
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": dom_e["hbm_gbs"], "peak": peak,
+                "peak_source": peak_src, "unit": "GB/s", "frac": dom_e["frac"],
+                "traffic": traffic_of(dom), "share_of_step": round(share[dom] / step_sum, 4),
+                "launches_per_step": sum(1 for k in per_ms if kernel_of(k) == dom),
+                "algorithmic_bytes_per_launch": 8.0 * n * n,
+                "timing": "isolated steady state: median over 5 groups of 10 back-to-back launches "
+                          "of this kernel alone (CUDA events around each group)",
                 "fp32": {"fma_per_px": macs / 4.0, "achieved_tflops": round(fp32, 2),
-                         "peak_tflops_nominal": round(fp32_peak, 1),
+                         "peak_tflops": round(fp32_peak, 1), "sms": sms,
                          "frac": round(fp32 / fp32_peak, 4)}}
 
-    # ---- C3 headline: cdf97 monolithic_star, 16384^2 (configs[2])
+    # ---- C3: 16384^2 (configs[2]) -- the north-star kernels
     c3 = None
     if args.c3:
         big = torch.rand((C3, C3), device=dev, generator=g, dtype=torch.float32)
         qb = torch.empty((4, C3 // 2, C3 // 2), device=dev, dtype=torch.float32)
         rb = torch.empty_like(big)
         c3 = {}
-        for sname in ("monolithic_star", "monolithic", "sweldens"):
-            sch = wl.build_scheme(sname, "cdf97")
-            for _ in range(3):
-                wl.forward(big, sch, out=qb)
-                wl.inverse(qb, "cdf97", scheme=sname, out=rb)
-            e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
-            tf = ti = 0.0
-            r = 10
-            for _ in range(r):
-                e[0].record(stream)
-                wl.forward(big, sch, out=qb)
-                e[1].record(stream)
-                wl.inverse(qb, "cdf97", scheme=sname, out=rb)
-                e[2].record(stream)
-                torch.cuda.synchronize()
-                tf += e[0].elapsed_time(e[1])
-                ti += e[1].elapsed_time(e[2])
-            for name, t in (("fwd", tf / r), ("inv", ti / r)):
-                gbs = 8.0 * C3 * C3 / (t * 1e-3) / 1e9
-                c3[f"cdf97/{sname}/{name}"] = {
-                    "ms": round(t, 4), "gpix_s": round(C3 * C3 / t / 1e6, 1),
-                    "ns_per_px": round(t * 1e6 / (C3 * C3), 6), "hbm_gbs": round(gbs, 1),
-                    "frac": round(gbs / peak, 4)}
+        for (w, s) in C3_PROGRAMS:
+            sch = wl.build_scheme(s, w)
+            tf = time_isolated(lambda: wl.forward(big, sch, out=qb), stream)
+            ti = time_isolated(lambda: wl.inverse(qb, w, scheme=s, out=rb), stream)
+            for d, t in (("fwd", tf), ("inv", ti)):
+                key = f"{w}/{s}/{d}"
+                c3[key] = prog_entry(t, C3, peak, traffic_of(f"c3/{key}"))
         del big, qb, rb
+        torch.cuda.empty_cache()
 
     # ---- e2e through the public API with pinned host buffers
     e2e = None
     if args.e2e_steps > 0:
-        # The reference-facing call shape: forward(const Image&) /
-        # inverse(const QuadGrid&) on HOST buffers (wl_dwt2_forward_host /
-        # wl_dwt2_inverse_host: row-chunk pipeline, H2D/kernels/D2H overlap).
-        h_img = torch.empty((n, n), dtype=torch.float32, pin_memory=True)
-        h_img.copy_(img.cpu())
-        h_q = torch.empty((4, n // 2, n // 2), dtype=torch.float32, pin_memory=True)
-        h_rec = torch.empty((n, n), dtype=torch.float32, pin_memory=True)
-
-        def e2e_step():
-            for (w, s) in programs:
-                wl.forward_host(h_img, schemes[(w, s)], out=h_q)    # host image -> host planes
-                wl.inverse_host(h_q, w, scheme=s, out=h_rec)        # host planes -> host image
-
-        e2e_step()
-        torch.cuda.synchronize()
-        barrier(ws)
-        t0 = time.perf_counter()
-        for _ in range(args.e2e_steps):
-            e2e_step()  # synchronous calls: results are in host memory on return
-        ems = barrier_max((time.perf_counter() - t0) * 1e3 / args.e2e_steps, ws)
-        bytes_img = 4 * n * n
-        e2e = {"value": ws * px_step / (ems * 1e-3) / 1e9, "unit": "GPixel/s",
-               "ms_per_step": ems, "h2d_bytes_per_step": 2 * len(programs) * bytes_img,
-               "d2h_bytes_per_step": 2 * len(programs) * bytes_img,
-               "steps": args.e2e_steps,
-               "api": "forward_host / inverse_host (pinned host float32 buffers; wall clock "
-                      "around synchronous calls); byte counts are the image/plane tensors, "
-                      "the strip halo rows add <=1.2% H2D"}
+        e2e = run_e2e(args, wl, ws, img, schemes, px_step)
 
     c4 = run_c4(args, wl, ws, rank, peak) if args.c4 else None
     c5 = run_c5(args, wl, ws, rank, peak) if args.c5 else None
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
-        cpu = cpu_baseline(args)
+        cpu = cpu_baseline(args, per_ms)
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "GPixel/s", "n_gpus": ws,
@@ -389,21 +414,101 @@ def run_gpu(args):
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
                 "dtype": "f32", "data": "synthetic",
                 "ns_per_pixel": ms * 1e6 / px_step,
-                "config": {"workload": f"configs[1]: every scheme x {{cdf53, cdf97}}, "
-                                       f"single-level forward + that scheme's inverse, "
-                                       f"{n}x{n} float32 per rank, periodic, no scaling",
-                           "size": n, "programs": len(programs),
-                           "pixels_per_step_per_rank": px_step,
-                           "l2": "inputs (256 MiB) larger than L2 (126 MB); no flush",
-                           "parallelism": f"independent images, {ws} rank(s)"},
+                "config": workload_config(n, ws),
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches, "gpu_launches_per_step": launches / args.steps,
-                "clocks": clk.summary(), "c3": c3, "c4": c4, "c5": c5, "per_scheme": per}
+                "clocks": clocks, "c4": c4, "c5": c5,
+                "per_scheme_unit": "[ms, GPix/s, frac of copy peak] per launch, isolated steady "
+                                   "state (median of 5 groups of 10 back-to-back launches)",
+                "per_scheme": per,
+                "north_star": north_star(c3, c4, c5)}
         print(json.dumps(line), flush=True)
     if ws > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
     return 0
+
+
+def north_star(c3, c4, c5):
+    """Compact configs[2..4] summary, emitted LAST in the line."""
+    out = {}
+    if c3:
+        out["c3_unit"] = "16384^2: [ms, frac of copy peak, ncu DRAM bytes / algorithmic]"
+        out["c3"] = {k: [v["ms"], v["frac"], v.get("traffic_ratio")] for k, v in c3.items()}
+    if c4:
+        out["c4"] = {"ms": round(c4["ms"], 3), "gpix_s": round(c4["value"], 1),
+                     "frac_per_gpu": round(c4["frac_per_gpu"], 4), "ranks": c4["ranks"]}
+    if c5:
+        out["c5"] = {w: {"ms": round(c5[w]["ms"], 2), "gpix_s": round(c5[w]["value"], 1),
+                         "frac_per_gpu": round(c5[w]["frac_per_gpu"], 4)}
+                     for w in ("cdf53", "cdf97") if w in c5}
+    return out
+
+
+def pcie_probe(nbytes):
+    """The box's pinned-copy ceiling: H2D alone, D2H alone, both at once."""
+    import torch
+    h_a = torch.empty(nbytes // 4, dtype=torch.float32, pin_memory=True)
+    h_b = torch.empty(nbytes // 4, dtype=torch.float32, pin_memory=True)
+    d_a = torch.empty(nbytes // 4, device="cuda")
+    d_b = torch.empty(nbytes // 4, device="cuda")
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+
+    def timed(fn):
+        fn()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        return (time.perf_counter() - t0) / 3
+
+    def both():
+        with torch.cuda.stream(s1):
+            d_a.copy_(h_a, non_blocking=True)
+        with torch.cuda.stream(s2):
+            h_b.copy_(d_b, non_blocking=True)
+    t_h2d = timed(lambda: d_a.copy_(h_a, non_blocking=True))
+    t_d2h = timed(lambda: h_b.copy_(d_b, non_blocking=True))
+    t_both = timed(both)
+    return {"h2d_gbs": round(nbytes / t_h2d / 1e9, 1), "d2h_gbs": round(nbytes / t_d2h / 1e9, 1),
+            "duplex_gbs_per_direction": round(nbytes / t_both / 1e9, 1), "bytes": nbytes}
+
+
+def run_e2e(args, wl, ws, img, schemes, px_step):
+    """The reference-facing call shape: forward(const Image&) /
+    inverse(const QuadGrid&) on HOST buffers (wl_dwt2_forward_host /
+    wl_dwt2_inverse_host: row-chunk pipeline, H2D/kernels/D2H overlap)."""
+    import torch
+    n = img.shape[0]
+    h_img = torch.empty((n, n), dtype=torch.float32, pin_memory=True)
+    h_img.copy_(img.cpu())
+    h_q = torch.empty((4, n // 2, n // 2), dtype=torch.float32, pin_memory=True)
+    h_rec = torch.empty((n, n), dtype=torch.float32, pin_memory=True)
+
+    def e2e_step():
+        for (w, s) in PROGRAMS:
+            wl.forward_host(h_img, schemes[(w, s)], out=h_q)    # host image -> host planes
+            wl.inverse_host(h_q, w, scheme=s, out=h_rec)        # host planes -> host image
+
+    e2e_step()
+    torch.cuda.synchronize()
+    barrier(ws)
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        e2e_step()  # synchronous calls: results are in host memory on return
+    ems = barrier_max((time.perf_counter() - t0) * 1e3 / args.e2e_steps, ws)
+    bytes_io = 2 * len(PROGRAMS) * 4 * n * n  # per direction per step
+    pcie = pcie_probe(4 * n * n)
+    gbs = bytes_io / (ems * 1e-3) / 1e9
+    return {"value": ws * px_step / (ems * 1e-3) / 1e9, "unit": "GPixel/s",
+            "ms_per_step": ems, "h2d_bytes_per_step": bytes_io, "d2h_bytes_per_step": bytes_io,
+            "steps": args.e2e_steps, "h2d_gbs": round(gbs, 1), "d2h_gbs": round(gbs, 1),
+            "pcie_ceiling": pcie,
+            "frac_of_duplex_ceiling": round(gbs / pcie["duplex_gbs_per_direction"], 3),
+            "api": "forward_host / inverse_host (pinned host float32 buffers; wall clock "
+                   "around synchronous calls); byte counts are the image/plane tensors, "
+                   "the strip halo rows add <=1.2% H2D"}
 
 
 def _timed(fn, steps, ws, stream):
@@ -450,7 +555,7 @@ def run_c4(args, wl, ws, rank, peak):
                         f"{n}x{n} float32, periodic, {ws} row strip(s) of {n // ws} rows, "
                         "halo rows pushed per level over peer memory (CUDA IPC)",
             "value": n * n / (ms * 1e-3) / 1e9, "unit": "GPixel/s (input pixels)",
-            "ms": ms, "ns_per_pixel": ms * 1e6 / (n * n), "scaling": "strong",
+            "ms": ms, "ns_per_pixel": ms * 1e6 / (n * n), "scaling": "strong", "ranks": ws,
             "algorithmic_bytes": algo, "hbm_gbs_per_gpu": gbs_per_gpu,
             "frac_per_gpu": gbs_per_gpu / peak}
 
@@ -499,25 +604,39 @@ def run_c5(args, wl, ws, rank, peak):
     return out
 
 
-def cpu_baseline(args):
-    """The unmodified reference (oracle/_ref) on this host: bounded sample."""
+def cpu_baseline(args, gpu_ms):
+    """The unmodified reference (oracle/_ref) on this host at the FULL
+    configs[1] size (n x n, float64) for the headline pair: cdf53 Monolithic
+    and cdf97 Monolithic* forward (transform.cpp:163) + the reference inverse
+    (transform.cpp:178), next to the GPU's isolated times of the same
+    programs (same size, same input distribution)."""
     try:
         import numpy as np
-        from oracle.oracle import Oracle, RefLib
-        try:
-            ref, kind = RefLib(), "reference"
-        except FileNotFoundError:
-            ref, kind = Oracle(), "port"
-        n = args.ref_size
+        ref, kind, cores = _ref_lib()
+        n = args.size
         img = np.random.default_rng(12345).random((n, n))
-        t0 = time.perf_counter()
-        px = reference_step_sample(ref, img)
-        dt = time.perf_counter() - t0
-        cores = ref.worker_count() if kind == "reference" else 1
-        return {"value": px / dt / 1e9, "unit": "GPixel/s", "cores": cores, "kind": kind,
-                "ns_per_pixel": 1e9 * dt / px, "seconds": dt,
-                "sample": f"{n}x{n} float64, every scheme x {{cdf53,cdf97}} forward + "
-                          f"reference inverse (1 pass each), periodic, {cores} threads"}
+        same, px, tot = {}, 0, 0.0
+        for (w, s) in CPU_FULL:
+            t0 = time.perf_counter()
+            qd = ref.forward(img, w, s, "periodic", False)
+            t1 = time.perf_counter()
+            ref.inverse(qd, w, "periodic", False)
+            t2 = time.perf_counter()
+            del qd
+            for d, t in (("fwd", t1 - t0), ("inv", t2 - t1)):
+                key = f"{w}/{s}/{d}"
+                g_ms = gpu_ms.get(key)
+                same[key] = {"cpu_ms": round(1e3 * t, 1), "cpu_ns_per_px": round(1e9 * t / img.size, 2),
+                             "gpu_ms": round(g_ms, 5) if g_ms else None,
+                             "gpu_over_cpu": round(1e3 * t / g_ms, 1) if g_ms else None}
+            px += 2 * img.size
+            tot += t2 - t0
+        return {"value": px / tot / 1e9, "unit": "GPixel/s", "cores": cores, "kind": kind,
+                "ns_per_pixel": 1e9 * tot / px, "seconds": round(tot, 2),
+                "sample": f"{n}x{n} float64 (the full configs[1] size), uniform[0,1) numpy seed "
+                          f"12345: cdf53 monolithic and cdf97 monolithic_star, forward + "
+                          f"reference inverse, 1 pass each, periodic, {cores} threads",
+                "same_config": same}
     except Exception as e:  # report, never fake
         return {"value": None, "unit": "GPixel/s", "cores": None, "kind": "unavailable",
                 "sample": f"error: {e}"}
@@ -530,8 +649,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--size", type=int, default=SIZE)
-    ap.add_argument("--ref-size", type=int, default=512)
-    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--ref-rows", type=int, default=256,
+                    help="reference arm: rows of the 8192-wide band timed per step")
+    ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-c3", dest="c3", action="store_false")
     ap.add_argument("--no-c4", dest="c4", action="store_false")
     ap.add_argument("--no-c5", dest="c5", action="store_false")

@@ -7,7 +7,10 @@
 // build_scheme, count_macs, count_barriers), wavelets.hpp:21-32 (WaveletSpec,
 // get_wavelet) and subband_io.hpp:45-46 (boundary_name, parse_boundary), with
 // the same value semantics (host float64 buffers) and the same exception
-// classes. Every transform runs on the GPU through the C-ABI of wl_dwt.h:
+// classes. Scheme carries its step sequence (Step{matrix, needs_barrier,
+// label}, schemes.hpp:34-45) and Convolution filters, read from the
+// library's build_scheme tables; apply_step (transform.hpp:57-60) runs one
+// StepMatrix on the GPU. Every transform runs on the GPU through the C-ABI of wl_dwt.h:
 // samples are converted to float32, copied to device memory, transformed by
 // the sm_100a kernels and copied back. There is no CPU fallback.
 //
@@ -18,6 +21,7 @@
 
 #include <array>
 #include <cstddef>
+#include <map>
 #include <optional>
 #include <stdexcept>
 #include <string>
@@ -67,9 +71,79 @@ struct WaveletSpec {
     double zeta = 1.0;
 };
 
+// polyphase.hpp:24-38
+enum class MatrixKind { T_H, T_V, S_H, S_V, T_I, R_I, S_I, T_E, R_E, S_E, T_MONO, S_MONO, N_FULL };
+
+// laurent.hpp:75-115, reduced to what a step-walking caller reads: the terms
+// c * z_m^km * z_n^kn of one matrix entry, keyed (k_m, k_n) in map order,
+// coefficients as double (the reference's Coeff::to_double()).
+struct LaurentPoly2 {
+    using Exp = std::pair<int, int>;
+    std::map<Exp, double> terms_;
+    const std::map<Exp, double>& terms() const { return terms_; }
+    bool is_zero() const { return terms_.empty(); }
+    bool is_one() const {
+        return terms_.size() == 1 && terms_.begin()->first == Exp{0, 0} &&
+               terms_.begin()->second == 1.0;
+    }
+    double at(int km, int kn) const {
+        const auto it = terms_.find({km, kn});
+        return it == terms_.end() ? 0.0 : it->second;
+    }
+    void set_term(int km, int kn, double c) {
+        if (c == 0.0) terms_.erase({km, kn});
+        else terms_[{km, kn}] = c;
+    }
+    int tap_count() const { return static_cast<int>(terms_.size()); }
+};
+
+// polyphase.hpp:45-68
+class StepMatrix {
+public:
+    explicit StepMatrix(MatrixKind kind = MatrixKind::N_FULL) : kind_(kind) {}
+    static StepMatrix identity() {
+        StepMatrix m;
+        for (int k = 0; k < 4; ++k) m.m_[k * 4 + k].set_term(0, 0, 1.0);
+        return m;
+    }
+    MatrixKind kind() const { return kind_; }
+    void set_kind(MatrixKind k) { kind_ = k; }
+    bool needs_barrier() const { return needs_barrier_; }
+    void set_needs_barrier(bool b) { needs_barrier_ = b; }
+    const LaurentPoly2& entry(int row, int col) const { return m_.at(row * 4 + col); }
+    void set_entry(int row, int col, const LaurentPoly2& p) { m_.at(row * 4 + col) = p; }
+    LaurentPoly2& mutable_entry(int row, int col) { return m_.at(row * 4 + col); }
+    bool is_identity() const {
+        for (int r = 0; r < 4; ++r)
+            for (int c = 0; c < 4; ++c)
+                if (r == c ? !entry(r, c).is_one() : !entry(r, c).is_zero()) return false;
+        return true;
+    }
+
+private:
+    std::array<LaurentPoly2, 16> m_;
+    MatrixKind kind_;
+    bool needs_barrier_ = true;
+};
+
+// schemes.hpp:34-38
+struct Step {
+    StepMatrix matrix;
+    bool needs_barrier = true;
+    std::string label;  // e.g. "T_H", "N(P1,U1)"
+};
+
+// wavelets.hpp:50-53
+struct ConvFilters {
+    LaurentPoly2 f_ll, f_hl, f_lh, f_hh;
+};
+
+// schemes.hpp:40-45
 struct Scheme {
     SchemeKind kind = SchemeKind::Sweldens;
     WaveletSpec wavelet;
+    std::vector<Step> steps;                  // empty for Convolution
+    std::optional<ConvFilters> conv_filters;  // set only for Convolution
 };
 
 struct PyramidLevel {
@@ -166,7 +240,79 @@ inline std::optional<BoundaryMode> parse_boundary(const std::string& s) {
     return std::nullopt;
 }
 
-inline Scheme build_scheme(SchemeKind kind, const WaveletSpec& w) { return Scheme{kind, w}; }
+// schemes.cpp:146-174: the step sequence as the library's tables hold it
+// (generated from the same algebra, checked against the reference's dump).
+inline Scheme build_scheme(SchemeKind kind, const WaveletSpec& w) {
+    Scheme s;
+    s.kind = kind;
+    s.wavelet = w;
+    const int ki = static_cast<int>(kind);
+    const int n = wl_scheme_nsteps(w.id, ki);
+    if (n < 0) detail::check(WL_EINVAL);
+    for (int k = 0; k < n; ++k) {
+        int mk = 0, nb = 0, nt = 0;
+        char label[64];
+        detail::check(wl_scheme_step(w.id, ki, k, &mk, &nb, &nt, label, sizeof label));
+        std::vector<int> rows(nt), cols(nt), km(nt), kn(nt);
+        std::vector<double> co(nt);
+        wl_scheme_step_terms(w.id, ki, k, rows.data(), cols.data(), km.data(), kn.data(),
+                             co.data(), nt);
+        Step st;
+        st.matrix.set_kind(static_cast<MatrixKind>(mk));
+        st.matrix.set_needs_barrier(nb != 0);
+        for (int t = 0; t < nt; ++t) st.matrix.mutable_entry(rows[t], cols[t]).set_term(km[t], kn[t], co[t]);
+        st.needs_barrier = nb != 0;
+        st.label = label;
+        s.steps.push_back(std::move(st));
+    }
+    if (kind == SchemeKind::Convolution) {
+        ConvFilters f;
+        LaurentPoly2* dst[4] = {&f.f_ll, &f.f_hl, &f.f_lh, &f.f_hh};
+        for (int which = 0; which < 4; ++which) {
+            const int nt = wl_scheme_conv_filter(w.id, which, nullptr, nullptr, nullptr, 0);
+            if (nt < 0) detail::check(WL_EINVAL);
+            std::vector<int> km(nt), kn(nt);
+            std::vector<double> co(nt);
+            wl_scheme_conv_filter(w.id, which, km.data(), kn.data(), co.data(), nt);
+            for (int t = 0; t < nt; ++t) dst[which]->set_term(km[t], kn[t], co[t]);
+        }
+        s.conv_filters = f;
+    }
+    return s;
+}
+
+// polyphase.cpp:301-340: the four 2-D filters reassembled into one 4x4
+// polyphase matrix.
+inline StepMatrix conv_polyphase_matrix(const ConvFilters& f) {
+    StepMatrix m(MatrixKind::N_FULL);
+    const LaurentPoly2* rows[4] = {&f.f_ll, &f.f_hl, &f.f_lh, &f.f_hh};
+    for (int target = 0; target < 4; ++target) {
+        const bool col_high = target == HL || target == HH, row_high = target == LH || target == HH;
+        for (const auto& [e, c] : rows[target]->terms()) {
+            const int km = e.first, kn = e.second;
+            int a, b;
+            bool codd, rodd;
+            if (!col_high) { codd = km % 2 != 0; a = codd ? (km + 1) / 2 : km / 2; }
+            else { codd = km % 2 == 0; a = codd ? km / 2 : (km - 1) / 2; }
+            if (!row_high) { rodd = kn % 2 != 0; b = rodd ? (kn + 1) / 2 : kn / 2; }
+            else { rodd = kn % 2 == 0; b = rodd ? kn / 2 : (kn - 1) / 2; }
+            LaurentPoly2& en = m.mutable_entry(target, (rodd ? 2 : 0) + (codd ? 1 : 0));
+            en.set_term(a, b, en.at(a, b) + c);
+        }
+    }
+    return m;
+}
+
+// schemes.cpp:221-228
+inline std::vector<StepMatrix> scheme_step_matrices(const Scheme& s) {
+    if (s.kind == SchemeKind::Convolution) {
+        if (!s.conv_filters) throw std::invalid_argument("convolution scheme without filters");
+        return {conv_polyphase_matrix(*s.conv_filters)};
+    }
+    std::vector<StepMatrix> out;
+    for (const Step& st : s.steps) out.push_back(st.matrix);
+    return out;
+}
 
 inline long count_macs(const Scheme& s) {
     long macs = 0;
@@ -212,6 +358,34 @@ inline Image polyphase_merge(const QuadGrid& q) {
             img.at(2 * r + 1, 2 * c + 1) = q.at(HH, r, c);
         }
     return img;
+}
+
+// transform.cpp:100-125: one step on the GPU (float32), out of place.
+inline QuadGrid apply_step(const QuadGrid& q, const StepMatrix& step, BoundaryMode b) {
+    const std::size_t n = static_cast<std::size_t>(q.w) * q.h;
+    for (const auto& p : q.planes)
+        if (p.size() != n) throw std::invalid_argument("quad grid plane size mismatch");
+    std::vector<int> rows, cols, km, kn;
+    std::vector<double> co;
+    for (int r = 0; r < 4; ++r)
+        for (int c = 0; c < 4; ++c)
+            for (const auto& [e, v] : step.entry(r, c).terms()) {
+                rows.push_back(r);
+                cols.push_back(c);
+                km.push_back(e.first);
+                kn.push_back(e.second);
+                co.push_back(v);
+            }
+    detail::DevBuf in(4 * n), out(4 * n);
+    for (int c = 0; c < 4; ++c) in.upload(q.planes[c].data(), n, c * n);
+    detail::check(wl_apply_step(in.p, in.p + n, in.p + 2 * n, in.p + 3 * n, q.w, q.h, q.w,
+                                static_cast<int>(co.size()), rows.data(), cols.data(), km.data(),
+                                kn.data(), co.data(), detail::boundary_id(b), out.p, out.p + n,
+                                out.p + 2 * n, out.p + 3 * n, q.w, nullptr));
+    detail::cuda(cudaDeviceSynchronize(), "apply_step");
+    QuadGrid o(q.w, q.h);
+    for (int c = 0; c < 4; ++c) out.download(o.planes[c].data(), n, c * n);
+    return o;
 }
 
 // transform.cpp:163-176. Host in / host out through wl_dwt2_forward_host

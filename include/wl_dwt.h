@@ -49,6 +49,39 @@ const char* wl_version(void);
 int wl_scheme_info(int wavelet, int scheme, int direction, int* barriers, long* macs,
                    int* epochs, int* halo);
 
+/* ------------------------------------------------- scheme structure (host)
+ * The result of build_scheme(kind, wavelet) (schemes.cpp:146-174,
+ * schemes.hpp:34-45) for callers that walk Scheme::steps (e.g. parsim.cpp:
+ * 250,285-286,337-338). matrix_kind follows MatrixKind (polyphase.hpp:24-38:
+ * T_H=0 ... N_FULL=12). A term is one Laurent monomial of entry (row, col):
+ * coefficient * z_m^km * z_n^kn; terms come in the reference's order (row,
+ * col, then std::map order of (km, kn)). */
+/* Number of steps (0 for Convolution), -1 for unknown ids. */
+int wl_scheme_nsteps(int wavelet, int scheme);
+/* Step k: MatrixKind, needs_barrier, number of terms, label (NUL-terminated,
+ * truncated to label_cap). Any output pointer may be NULL. */
+int wl_scheme_step(int wavelet, int scheme, int k, int* matrix_kind, int* needs_barrier,
+                   int* nterms, char* label, int label_cap);
+/* Terms of step k into arrays of `cap` entries (any may be NULL). Returns the
+ * number of terms (call with cap = 0 to size the arrays), -1 on bad ids. */
+int wl_scheme_step_terms(int wavelet, int scheme, int k, int* rows, int* cols, int* km, int* kn,
+                         double* coeff, int cap);
+/* Convolution: 2-D analysis filter `which` (0 f_ll, 1 f_hl, 2 f_lh, 3 f_hh;
+ * wavelets.cpp:80-88, wavelets.hpp:50-53) as km/kn/coeff terms in map order.
+ * Returns the number of taps (cap = 0 to size), -1 on bad ids. */
+int wl_scheme_conv_filter(int wavelet, int which, int* km, int* kn, double* coeff, int cap);
+
+/* One step matrix on device planes, out of place: replaces `QuadGrid
+ * apply_step(const QuadGrid&, const StepMatrix&, BoundaryMode)`
+ * (transform.hpp:57-60, transform.cpp:100-125). The matrix is given as
+ * `nterms` HOST terms (rows/cols/km/kn/coeff as above, <= 512); a term reads
+ * the source plane at (r - kn, c - km) resolved under `boundary`. Sums per
+ * destination in (source, map) order with unfused multiply/add, float32. */
+int wl_apply_step(const float* ll, const float* hl, const float* lh, const float* hh, int qw,
+                  int qh, long pitch, int nterms, const int* rows, const int* cols, const int* km,
+                  const int* kn, const double* coeff, int boundary, float* out_ll, float* out_hl,
+                  float* out_lh, float* out_hh, long out_pitch, void* stream);
+
 /* transform.cpp:59-72 resolve_index (host-side helper). */
 int wl_resolve_index(int i, int n, int boundary);
 

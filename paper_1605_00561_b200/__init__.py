@@ -83,6 +83,13 @@ def lib() -> ctypes.CDLL:
         if hasattr(l, "wl_set_level_fusion"):  # absent in A/B builds of older sources
             l.wl_set_level_fusion.argtypes = [i]
         l.wl_launch_count.restype = lg
+        ip, dp = ctypes.POINTER(i), ctypes.POINTER(ctypes.c_double)
+        l.wl_scheme_nsteps.argtypes = [i, i]
+        l.wl_scheme_step.argtypes = [i, i, i, ip, ip, ip, ctypes.c_char_p, i]
+        l.wl_scheme_step_terms.argtypes = [i, i, i, ip, ip, ip, ip, dp, i]
+        l.wl_scheme_conv_filter.argtypes = [i, i, ip, ip, dp, i]
+        l.wl_apply_step.argtypes = [fp, fp, fp, fp, i, i, lg, i, ip, ip, ip, ip, dp, i, fp, fp,
+                                    fp, fp, lg, vp]
         _lib = l
     return _lib
 
@@ -157,15 +164,82 @@ def get_wavelet(name: str) -> WaveletSpec:
     return WaveletSpec(w.name, WAVELETS.index(w.name), w.zeta)
 
 
+MATRIX_KINDS = ("T_H", "T_V", "S_H", "S_V", "T_I", "R_I", "S_I", "T_E", "R_E", "S_E",
+                "T_MONO", "S_MONO", "N_FULL")  # polyphase.hpp:24-38 MatrixKind
+
+
+@dataclass(frozen=True)
+class StepMatrix:
+    """polyphase.hpp:45-68: 4x4 Laurent matrix over [LL, HL, LH, HH];
+    entries[(row, col)] = {(k_m, k_n): coefficient} (double)."""
+    entries: dict
+    kind: str = "N_FULL"
+    needs_barrier: bool = True
+
+    def entry(self, row: int, col: int) -> dict:
+        return self.entries.get((row, col), {})
+
+    def is_identity(self) -> bool:
+        return all((r == c and p == {(0, 0): 1.0}) or (r != c and not p)
+                   for (r, c), p in self.entries.items()) and \
+            all(self.entries.get((k, k)) == {(0, 0): 1.0} for k in range(4))
+
+
+@dataclass(frozen=True)
+class Step:
+    """schemes.hpp:34-38."""
+    matrix: StepMatrix
+    needs_barrier: bool
+    label: str
+
+
 @dataclass(frozen=True)
 class Scheme:
-    """schemes.hpp:40-45, reduced to the selection the kernels need."""
+    """schemes.hpp:40-45: kind + wavelet; `steps` / `conv_filters` are read
+    from the library's build_scheme tables (schemes.cpp:146-174)."""
     kind: int
     wavelet: WaveletSpec
 
     @property
     def name(self) -> str:
         return SCHEMES[self.kind]
+
+    @property
+    def steps(self) -> list:
+        """The step sequence (empty for Convolution)."""
+        l, w = lib(), self.wavelet.index
+        n = l.wl_scheme_nsteps(w, self.kind)
+        if n < 0:
+            _check(WL_EINVAL)
+        out = []
+        for k in range(n):
+            mk, nb, nt = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+            label = ctypes.create_string_buffer(64)
+            _check(l.wl_scheme_step(w, self.kind, k, ctypes.byref(mk), ctypes.byref(nb),
+                                    ctypes.byref(nt), label, 64))
+            rows, cols, km, kn = [(ctypes.c_int * nt.value)() for _ in range(4)]
+            co = (ctypes.c_double * nt.value)()
+            l.wl_scheme_step_terms(w, self.kind, k, rows, cols, km, kn, co, nt.value)
+            ent = {}
+            for t in range(nt.value):
+                ent.setdefault((rows[t], cols[t]), {})[(km[t], kn[t])] = co[t]
+            out.append(Step(StepMatrix(ent, MATRIX_KINDS[mk.value], bool(nb.value)),
+                            bool(nb.value), label.value.decode()))
+        return out
+
+    @property
+    def conv_filters(self):
+        """(f_ll, f_hl, f_lh, f_hh) as {(k_m, k_n): c} (Convolution only, else None)."""
+        if SCHEMES[self.kind] != "convolution":
+            return None
+        l, out = lib(), []
+        for f in range(4):
+            n = l.wl_scheme_conv_filter(self.wavelet.index, f, None, None, None, 0)
+            km, kn = (ctypes.c_int * n)(), (ctypes.c_int * n)()
+            co = (ctypes.c_double * n)()
+            l.wl_scheme_conv_filter(self.wavelet.index, f, km, kn, co, n)
+            out.append({(km[t], kn[t]): co[t] for t in range(n)})
+        return tuple(out)
 
     def info(self, direction: int = 0) -> dict:
         b, m, e, h = ctypes.c_int(), ctypes.c_long(), ctypes.c_int(), ctypes.c_int()
@@ -178,6 +252,72 @@ def build_scheme(kind, wavelet) -> Scheme:
     """schemes.cpp:146-174 (selection only)."""
     w = wavelet if isinstance(wavelet, WaveletSpec) else get_wavelet(wavelet)
     return Scheme(_index(SCHEMES, kind, "scheme"), w)
+
+
+def conv_polyphase_matrix(filters) -> StepMatrix:
+    """polyphase.cpp:301-340: the polyphase reassembly of the four 2-D
+    analysis filters into one 4x4 matrix."""
+    ent = {}
+    for target, f in enumerate(filters):
+        col_high, row_high = target in (1, 3), target in (2, 3)
+        for (km, kn), c in f.items():
+            if not col_high:
+                codd = km % 2 != 0
+                a = (km + 1) // 2 if codd else km // 2
+            else:
+                codd = km % 2 == 0
+                a = km // 2 if codd else (km - 1) // 2
+            if not row_high:
+                rodd = kn % 2 != 0
+                b = (kn + 1) // 2 if rodd else kn // 2
+            else:
+                rodd = kn % 2 == 0
+                b = kn // 2 if rodd else (kn - 1) // 2
+            src = (2 if rodd else 0) + (1 if codd else 0)
+            e = ent.setdefault((target, src), {})
+            e[(a, b)] = e.get((a, b), 0.0) + c
+    return StepMatrix(ent, "N_FULL", True)
+
+
+def scheme_step_matrices(s: Scheme) -> list:
+    """schemes.cpp:221-228: the scheme's own matrices, or the polyphase
+    reassembly of the four filters for Convolution."""
+    if SCHEMES[s.kind] == "convolution":
+        return [conv_polyphase_matrix(s.conv_filters)]
+    return [st.matrix for st in s.steps]
+
+
+def apply_step(q, step, boundary="periodic", out=None, stream=None):
+    """transform.cpp:100-125 on the GPU: out-of-place y_i = sum_j M_ij (*) x_j
+    for a (4, qh, qw) float32 CUDA tensor; `step` is a Step or StepMatrix.
+    Terms are summed in the reference's order (destination, source, then
+    exponent map order), multiply and add unfused."""
+    import torch
+    q = _dev_f32(q, "q").contiguous()
+    if q.dim() != 3 or q.shape[0] != 4:
+        raise ValueError("q must be (4, qh, qw)")
+    m = step.matrix if isinstance(step, Step) else step
+    rows, cols, km, kn, co = [], [], [], [], []
+    for (r, c) in sorted(m.entries):
+        for (a, b) in sorted(m.entries[(r, c)]):
+            rows.append(r)
+            cols.append(c)
+            km.append(a)
+            kn.append(b)
+            co.append(float(m.entries[(r, c)][(a, b)]))
+    n = len(co)
+    arr = lambda t, v: (t * max(n, 1))(*v)  # noqa: E731
+    _, qh, qw = q.shape
+    if out is None:
+        out = torch.empty_like(q)
+    _check(lib().wl_apply_step(q[0].data_ptr(), q[1].data_ptr(), q[2].data_ptr(),
+                               q[3].data_ptr(), qw, qh, qw, n, arr(ctypes.c_int, rows),
+                               arr(ctypes.c_int, cols), arr(ctypes.c_int, km),
+                               arr(ctypes.c_int, kn), arr(ctypes.c_double, co),
+                               _index(BOUNDARIES, boundary, "boundary"), out[0].data_ptr(),
+                               out[1].data_ptr(), out[2].data_ptr(), out[3].data_ptr(),
+                               out.stride(1), _stream_ptr(stream)))
+    return out
 
 
 def count_barriers(s: Scheme) -> int:

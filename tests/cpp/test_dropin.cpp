@@ -4,6 +4,8 @@
 // Built and run by tests/test_cpp_dropin.py on a GPU box. Exit 0 = all pass.
 #include <cmath>
 #include <cstdio>
+#include <cstring>
+#include <string>
 #include <random>
 #include <stdexcept>
 #include <vector>
@@ -11,6 +13,8 @@
 #include "wavelift_b200.hpp"
 
 extern "C" {
+long wlref_dump_scheme(int, int, char*, long);
+int wlref_apply_step(const double*, int, int, const int*, const double*, int, int, double*);
 int wlref_forward(const double*, int, int, int, int, int, int, double*);
 int wlref_inverse(const double*, int, int, int, int, int, double*);
 void wlref_random_image(int, int, unsigned, int, double*);
@@ -131,6 +135,81 @@ int main() {
         CHECK(resolve_index(-1, 4, BoundaryMode::symmetric) == 1 &&
                   resolve_index(-1, 4, BoundaryMode::periodic) == 3,
               "resolve_index");
+    }
+    // schemes.hpp:34-45: walk Scheme::steps like parsim.cpp:250,285-286 does --
+    // labels, needs_barrier flags and term counts equal the reference's
+    // build_scheme (its JSON dump, oracle/ref_capi.cpp), and every step run
+    // through apply_step equals the reference's apply_step on the same planes.
+    {
+        static const char* wn[] = {"cdf53", "cdf97", "dd137"};
+        for (int wi = 0; wi < 3; ++wi)
+            for (SchemeKind k : all_scheme_kinds()) {
+                const Scheme s = build_scheme(k, get_wavelet(wn[wi]));
+                const long len = wlref_dump_scheme(wi, static_cast<int>(k), nullptr, 0);
+                std::string js(static_cast<std::size_t>(len) + 1, '\0');
+                wlref_dump_scheme(wi, static_cast<int>(k), js.data(), len + 1);
+                std::size_t pos = 0;
+                int nref = 0;
+                for (const Step& st : s.steps) {
+                    const std::size_t lp = js.find("\"label\":\"", pos);
+                    CHECK(lp != std::string::npos, "%s/%s: fewer reference steps", wn[wi],
+                          scheme_name(k).c_str());
+                    if (lp == std::string::npos) break;
+                    const std::size_t l0 = lp + 9, l1 = js.find('"', l0);
+                    const std::string label = js.substr(l0, l1 - l0);
+                    const std::size_t bp = js.find("\"barrier\":", l1);
+                    const bool barrier = js[bp + 10] == '1';
+                    CHECK(label == st.label && barrier == st.needs_barrier &&
+                              barrier == st.matrix.needs_barrier(),
+                          "%s/%s step %d: %s/%d vs reference %s/%d", wn[wi],
+                          scheme_name(k).c_str(), nref, st.label.c_str(), st.needs_barrier,
+                          label.c_str(), barrier);
+                    pos = l1;
+                    ++nref;
+                }
+                CHECK(js.find("\"label\":\"", pos) == std::string::npos, "%s/%s: extra steps",
+                      wn[wi], scheme_name(k).c_str());
+                CHECK(k == SchemeKind::Convolution ? (s.steps.empty() && s.conv_filters &&
+                                                      s.conv_filters->f_ll.tap_count() > 0)
+                                                   : !s.conv_filters.has_value(),
+                      "conv filters");
+            }
+        // apply_step (transform.cpp:100-125): every Monolithic* / Polyphase step
+        const int qw = 40, qh = 26;
+        QuadGrid q(qw, qh);
+        std::mt19937 rng(7);
+        for (auto& p : q.planes)
+            for (double& v : p) v = static_cast<double>(rng() % 256) / 256.0;
+        std::vector<double> in4(4 * qw * qh);
+        for (int c = 0; c < 4; ++c) std::copy(q.planes[c].begin(), q.planes[c].end(), in4.begin() + c * qw * qh);
+        for (SchemeKind k : {SchemeKind::MonolithicStar, SchemeKind::Polyphase, SchemeKind::Explosive})
+            for (const Step& st : build_scheme(k, get_wavelet("cdf53")).steps)
+                for (BoundaryMode b : {BoundaryMode::periodic, BoundaryMode::symmetric}) {
+                    std::vector<int> idx;
+                    std::vector<double> co;
+                    for (int r = 0; r < 4; ++r)
+                        for (int c = 0; c < 4; ++c)
+                            for (const auto& [e, v] : st.matrix.entry(r, c).terms()) {
+                                idx.insert(idx.end(), {r, c, e.first, e.second});
+                                co.push_back(v);
+                            }
+                    std::vector<double> want(4 * qw * qh);
+                    CHECK(wlref_apply_step(in4.data(), qw, qh, idx.data(), co.data(),
+                                           static_cast<int>(co.size()),
+                                           b == BoundaryMode::periodic ? 0 : 1, want.data()) == 0,
+                          "reference apply_step");
+                    const QuadGrid got = apply_step(q, st.matrix, b);
+                    double m = 0;
+                    for (int c = 0; c < 4; ++c)
+                        for (int i = 0; i < qw * qh; ++i)
+                            m = std::max(m, std::abs(got.planes[c][i] - want[c * qw * qh + i]));
+                    // cdf53 on 8-bit dyadic planes: exact in float32
+                    CHECK(m == 0.0, "apply_step %s %s: %g", st.label.c_str(),
+                          boundary_name(b).c_str(), m);
+                }
+        const Scheme conv = build_scheme(SchemeKind::Convolution, get_wavelet("cdf97"));
+        const auto mats = scheme_step_matrices(conv);
+        CHECK(mats.size() == 1 && mats[0].entry(LL, LL).tap_count() > 0, "conv polyphase matrix");
     }
     std::printf("%d checks, %d failures\n", g_checks, g_fail);
     return g_fail ? 1 : 0;

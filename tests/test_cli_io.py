@@ -106,9 +106,10 @@ def test_cli_roundtrip_and_bench(tmp_path):
         r = run_cli("roundtrip", pgm, "--wavelet", w, "--scheme", "monolithic_star", "--levels", 3)
         assert r.returncode == 0 and "OK" in r.stdout, r.stdout + r.stderr
     # wavelift_main.cpp:196: the reference inverts with the wavelet-only
-    # (Sweldens) inverse, so a symmetric non-Sweldens roundtrip FAILs (exit 2)
-    # there; --scheme-inverse runs the scheme's own inverse kernel instead.
-    r = run_cli("roundtrip", pgm, "--scheme", "monolithic", "--boundary", "symmetric")
+    # (Sweldens) inverse, so a symmetric Polyphase roundtrip FAILs (exit 2)
+    # there (the oracle: max error 0.12); --scheme-inverse runs the scheme's
+    # own inverse kernel instead.
+    r = run_cli("roundtrip", pgm, "--scheme", "polyphase", "--boundary", "symmetric")
     assert r.returncode == 2 and "FAIL" in r.stdout and "note:" in r.stderr, r.stdout
     r = run_cli("roundtrip", pgm, "--scheme", "monolithic", "--boundary", "symmetric",
                 "--scheme-inverse")

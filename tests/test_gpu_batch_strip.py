@@ -199,6 +199,10 @@ def test_strip_pyramid_errors(wl):
         wl.StripPyramid(256, 64, 4, sch, 0, 2)  # deepest strip thinner than the halo
     with pytest.raises(ValueError):
         wl.StripPyramid(256, 256, 2, wl.build_scheme("sweldens", "dd137"), 0, 1)
+    # level widths 1200, 600, 300: the deepest level (300 = 4 mod 8 px) has no
+    # strip kernel -- rejected at create, before any exchange is enqueued
+    with pytest.raises(ValueError):
+        wl.StripPyramid(1200, 1024, 3, sch, 0, 2)
 
 
 def _ipc_worker(rank, n, port, out_path):
@@ -253,7 +257,9 @@ def test_host_buffer_transforms_equal_device_path(wl, wavelet):
     """forward_host / inverse_host (pipelined row chunks) == the device path,
     bit for bit, including sizes with several chunks and a ragged last one."""
     import torch
-    for (h, w) in [(8192 + 2 * 212, 1024), (512, 512), (34, 22)]:
+    # (4100, 4100): w = 4 mod 8 px with several chunks -- no strip kernel for
+    # that width, so the whole-image path must run (no WL_EINVAL)
+    for (h, w) in [(8192 + 2 * 212, 1024), (512, 512), (34, 22), (4100, 4100)]:
         img = rand((h, w), h)
         for s in ("monolithic_star", "sweldens", "convolution", "polyphase"):
             sch = wl.build_scheme(s, wavelet)

@@ -236,3 +236,21 @@ def test_launches_native_kernels(wl):
     torch.cuda.synchronize()
     # fast engine kernel + the interpreter's border frame (or 1 interpreter launch)
     assert 1 <= wl.launch_count() - n0 <= 2
+
+
+def test_apply_step_matches_reference(wl, ref):
+    """apply_step (transform.cpp:100-125) on the GPU vs the unmodified
+    reference's apply_step, for every step of several schemes (Scheme::steps
+    walked like parsim.cpp does), both boundaries, ragged sizes."""
+    for w in ("cdf53", "cdf97"):
+        for s in ("sweldens", "monolithic_star", "polyphase", "explosive", "iwahashi_star"):
+            for st in wl.build_scheme(s, w).steps:
+                for (qh, qw) in ((37, 50), (130, 260), (1, 1), (2, 3)):
+                    q = np.random.default_rng(qh * qw).integers(0, 256, (4, qh, qw)) / 256.0
+                    for b in BOUNDARIES:
+                        want = ref.apply_step(q, st.matrix.entries, b)
+                        got = host(wl.apply_step(gpu(q), st, b))
+                        if w == "cdf53":
+                            assert np.array_equal(got, want), (s, st.label, b, qh, qw)
+                        else:
+                            assert rel_err(got, want) <= TOL, (s, st.label, b, qh, qw)
