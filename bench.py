@@ -396,6 +396,30 @@ def run_gpu(args):
         del big, qb, rb
         torch.cuda.empty_cache()
 
+    # ---- unaligned shapes (w = 2 mod 4: odd plane widths, no TMA): the fast
+    # engine's direct-load variant, and the generic interpreter for scale
+    unaligned = None
+    if args.unaligned and ws == 1:
+        unaligned = {}
+        for m in (8190, 8194):
+            im = torch.rand((m, m), device=dev, generator=g, dtype=torch.float32)
+            qm = torch.empty((4, m // 2, m // 2), device=dev, dtype=torch.float32)
+            rm = torch.empty_like(im)
+            for (w, s) in CPU_FULL:
+                sch = wl.build_scheme(s, w)
+                tf = time_isolated(lambda: wl.forward(im, sch, out=qm), stream)
+                ti = time_isolated(lambda: wl.inverse(qm, w, scheme=s, out=rm), stream)
+                unaligned[f"{m}/{w}/{s}/fwd"] = prog_entry(tf, m, peak)
+                unaligned[f"{m}/{w}/{s}/inv"] = prog_entry(ti, m, peak)
+            if m == 8190:
+                prev = wl.set_engine(1)
+                sch = wl.build_scheme("monolithic_star", "cdf97")
+                t = time_isolated(lambda: wl.forward(im, sch, out=qm), stream, groups=3,
+                                  per_group=3)
+                wl.set_engine(prev)
+                unaligned["8190/cdf97/monolithic_star/fwd/interpreter"] = prog_entry(t, m, peak)
+            del im, qm, rm
+
     # ---- e2e through the public API with pinned host buffers
     e2e = None
     if args.e2e_steps > 0:
@@ -417,11 +441,11 @@ def run_gpu(args):
                 "config": workload_config(n, ws),
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches, "gpu_launches_per_step": launches / args.steps,
-                "clocks": clocks, "c4": c4, "c5": c5,
+                "clocks": clocks, "c4": c4, "c5": c5, "unaligned": unaligned,
                 "per_scheme_unit": "[ms, GPix/s, frac of copy peak] per launch, isolated steady "
                                    "state (median of 5 groups of 10 back-to-back launches)",
                 "per_scheme": per,
-                "north_star": north_star(c3, c4, c5)}
+                "north_star": north_star(c3, c4, c5, unaligned)}
         print(json.dumps(line), flush=True)
     if ws > 1:
         import torch.distributed as dist
@@ -429,9 +453,12 @@ def run_gpu(args):
     return 0
 
 
-def north_star(c3, c4, c5):
+def north_star(c3, c4, c5, unaligned=None):
     """Compact configs[2..4] summary, emitted LAST in the line."""
     out = {}
+    if unaligned:
+        out["unaligned_unit"] = "[ms, frac of copy peak] (8190^2 / 8194^2 images: no TMA)"
+        out["unaligned"] = {k: [v["ms"], v["frac"]] for k, v in unaligned.items()}
     if c3:
         out["c3_unit"] = "16384^2: [ms, frac of copy peak, ncu DRAM bytes / algorithmic]"
         out["c3"] = {k: [v["ms"], v["frac"], v.get("traffic_ratio")] for k, v in c3.items()}
@@ -475,12 +502,48 @@ def pcie_probe(nbytes):
             "duplex_gbs_per_direction": round(nbytes / t_both / 1e9, 1), "bytes": nbytes}
 
 
+def gpu_cpu_affinity(index):
+    """Host CPUs local to GPU `index` (nvidia-smi topo -m "CPU Affinity"), or
+    None. Pinned staging buffers touched from those CPUs land on the GPU's
+    NUMA node."""
+    try:
+        out = subprocess.run(["nvidia-smi", "topo", "-m"], capture_output=True, text=True,
+                             timeout=10).stdout.splitlines()
+        head = [h.strip() for h in out[0].split("\t")]
+        col = next(i for i, h in enumerate(head) if h.startswith("CPU Affinity"))
+        for line in out[1:]:
+            f = [x.strip() for x in line.split("\t")]
+            if f and f[0] == f"GPU{index}":
+                cpus = set()
+                for part in f[col].split(","):
+                    a, _, b = part.partition("-")
+                    cpus.update(range(int(a), int(b or a) + 1))
+                return cpus & os.sched_getaffinity(0) or None
+    except Exception:
+        return None
+    return None
+
+
 def run_e2e(args, wl, ws, img, schemes, px_step):
     """The reference-facing call shape: forward(const Image&) /
     inverse(const QuadGrid&) on HOST buffers (wl_dwt2_forward_host /
     wl_dwt2_inverse_host: row-chunk pipeline, H2D/kernels/D2H overlap)."""
     import torch
     n = img.shape[0]
+    # host side on the GPU's NUMA node (restored afterwards: the CPU
+    # reference runs on every core)
+    saved = os.sched_getaffinity(0)
+    local = gpu_cpu_affinity(torch.cuda.current_device())
+    if local:
+        os.sched_setaffinity(0, local)
+    try:
+        return _run_e2e(args, wl, ws, img, schemes, px_step, n, local)
+    finally:
+        os.sched_setaffinity(0, saved)
+
+
+def _run_e2e(args, wl, ws, img, schemes, px_step, n, local):
+    import torch
     h_img = torch.empty((n, n), dtype=torch.float32, pin_memory=True)
     h_img.copy_(img.cpu())
     h_q = torch.empty((4, n // 2, n // 2), dtype=torch.float32, pin_memory=True)
@@ -506,6 +569,8 @@ def run_e2e(args, wl, ws, img, schemes, px_step):
             "steps": args.e2e_steps, "h2d_gbs": round(gbs, 1), "d2h_gbs": round(gbs, 1),
             "pcie_ceiling": pcie,
             "frac_of_duplex_ceiling": round(gbs / pcie["duplex_gbs_per_direction"], 3),
+            "host_cpus": (f"{len(local)} CPUs local to the GPU (nvidia-smi topo)" if local
+                          else "all (GPU affinity unknown)"),
             "api": "forward_host / inverse_host (pinned host float32 buffers; wall clock "
                    "around synchronous calls); byte counts are the image/plane tensors, "
                    "the strip halo rows add <=1.2% H2D"}
@@ -536,8 +601,14 @@ def run_c4(args, wl, ws, rank, peak):
         sp = wl.strip_pyramid_distributed(None, n, n, levels, sch)
     else:
         sp = wl.StripPyramid(n, n, levels, sch)
-    g = torch.Generator(device="cuda").manual_seed(4000 + rank)
-    sp.input.copy_(torch.rand(sp.input.shape, device="cuda", generator=g))
+    # deterministic content by GLOBAL pixel coordinates: the same image for
+    # every rank count, so the checksum is comparable across N
+    rows = n // ws
+    r_idx = torch.arange(rank * rows, (rank + 1) * rows, device="cuda", dtype=torch.int64)
+    c_idx = torch.arange(n, device="cuda", dtype=torch.int64)
+    h_ = (r_idx[:, None] * 1103515245 + c_idx[None, :] * 12345 + 2654435761) % 2147483647
+    sp.input.copy_((h_ % 65536).float() / 65536.0)
+    del h_
     out = torch.empty(sp.slice_elems(), device="cuda")
     stream = torch.cuda.current_stream()
     torch.cuda.synchronize()
@@ -547,6 +618,13 @@ def run_c4(args, wl, ws, rank, peak):
     torch.cuda.synchronize()
     ms = _timed(lambda: sp.forward(out), max(args.steps, 5), ws, stream)
     sp.check()
+    checksum = out.double().sum()
+    if ws > 1:
+        import torch.distributed as dist
+        cs = checksum.reshape(1).to("cuda" if dist.get_backend() == "nccl" else "cpu")
+        dist.all_reduce(cs)
+        checksum = cs[0]
+    checksum = float(checksum)
     algo = 8.0 * n * n * sum(4.0 ** -l for l in range(levels))
     gbs_per_gpu = algo / ws / (ms * 1e-3) / 1e9
     sp.close()
@@ -556,6 +634,7 @@ def run_c4(args, wl, ws, rank, peak):
                         "halo rows pushed per level over peer memory (CUDA IPC)",
             "value": n * n / (ms * 1e-3) / 1e9, "unit": "GPixel/s (input pixels)",
             "ms": ms, "ns_per_pixel": ms * 1e6 / (n * n), "scaling": "strong", "ranks": ws,
+            "checksum": checksum,
             "algorithmic_bytes": algo, "hbm_gbs_per_gpu": gbs_per_gpu,
             "frac_per_gpu": gbs_per_gpu / peak}
 
@@ -659,6 +738,7 @@ def main():
     ap.add_argument("--c5-images", type=int, default=4096)
     ap.add_argument("--c5-pool", type=int, default=256)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-unaligned", dest="unaligned", action="store_false")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

@@ -224,7 +224,13 @@ int wl_set_engine(int engine);
  * environment WL_FUSE=1 turns it on). Results are bit-identical either way.
  * Returns the previous value. Process-global. */
 int wl_set_level_fusion(int on);
-/* Number of kernel launches this library issued so far (process-global). */
+/* Pyramid drivers (wl_dwt2_pyramid_*): a call repeated with identical
+ * arguments is replayed from a CUDA graph captured on its second occurrence
+ * (one cudaGraphLaunch instead of one launch per level). 1 = on (default;
+ * environment WL_GRAPHS=0 turns it off). Returns the previous value. */
+int wl_set_graphs(int on);
+/* Number of kernel launches this library issued so far (process-global;
+ * a graph replay counts its kernel nodes). */
 long wl_launch_count(void);
 
 #ifdef __cplusplus

@@ -83,6 +83,8 @@ def lib() -> ctypes.CDLL:
         if hasattr(l, "wl_set_level_fusion"):  # absent in A/B builds of older sources
             l.wl_set_level_fusion.argtypes = [i]
         l.wl_launch_count.restype = lg
+        if hasattr(l, "wl_set_graphs"):
+            l.wl_set_graphs.argtypes = [i]
         ip, dp = ctypes.POINTER(i), ctypes.POINTER(ctypes.c_double)
         l.wl_scheme_nsteps.argtypes = [i, i]
         l.wl_scheme_step.argtypes = [i, i, i, ip, ip, ip, ctypes.c_char_p, i]
@@ -115,6 +117,12 @@ def set_engine(engine: int) -> int:
 def set_level_fusion(on: bool) -> bool:
     """Fuse consecutive forward pyramid levels into one launch (default off)."""
     return bool(lib().wl_set_level_fusion(1 if on else 0))
+
+
+def set_graphs(on: bool) -> bool:
+    """Graph replay of repeated pyramid calls (wl_set_graphs); returns the
+    previous setting."""
+    return bool(lib().wl_set_graphs(int(bool(on))))
 
 
 def launch_count() -> int:
@@ -419,15 +427,21 @@ class Pyramid:
 
 
 def multi_level_forward(img, scheme: Scheme, levels: int, boundary="periodic",
-                        apply_scaling=False, stream=None) -> Pyramid:
-    """transform.cpp:198-227."""
+                        apply_scaling=False, stream=None, out=None, scratch=None) -> Pyramid:
+    """transform.cpp:198-227. `out` (flat, w*h floats) and `scratch` may be
+    passed to reuse buffers (repeated calls with the same buffers replay a
+    CUDA graph, see set_graphs)."""
     import torch
     img = _dev_f32(img, "img").contiguous()
     h, w = img.shape
     n = lib().wl_pyramid_elems(w, h, levels)
-    flat = torch.empty(max(n, 1), device=img.device, dtype=torch.float32)
-    scratch = torch.empty(max(lib().wl_pyramid_scratch_elems(w, h, levels), 1),
-                          device=img.device, dtype=torch.float32)
+    flat = out if out is not None else torch.empty(max(n, 1), device=img.device,
+                                                   dtype=torch.float32)
+    if out is not None and (_dev_f32(out, "out").numel() < n or not out.is_contiguous()):
+        raise ValueError("out must be a contiguous float32 CUDA tensor of w*h elements")
+    need = lib().wl_pyramid_scratch_elems(w, h, levels)
+    if scratch is None or scratch.numel() < need:
+        scratch = torch.empty(max(need, 1), device=img.device, dtype=torch.float32)
     _check(lib().wl_dwt2_pyramid_forward(img.data_ptr(), w, h, levels, scheme.wavelet.index,
                                          scheme.kind, _index(BOUNDARIES, boundary, "boundary"),
                                          int(bool(apply_scaling)), flat.data_ptr(),
@@ -436,8 +450,9 @@ def multi_level_forward(img, scheme: Scheme, levels: int, boundary="periodic",
 
 
 def multi_level_inverse(pyr: Pyramid, wavelet, boundary="periodic", undo_scaling=False,
-                        scheme=None, stream=None):
-    """transform.cpp:229-256."""
+                        scheme=None, stream=None, out=None, scratch=None):
+    """transform.cpp:229-256 (`out` / `scratch` reusable as in
+    multi_level_forward)."""
     import torch
     w = wavelet if isinstance(wavelet, WaveletSpec) else get_wavelet(wavelet)
     kind = 0 if scheme is None else (scheme.kind if isinstance(scheme, Scheme)
@@ -445,10 +460,11 @@ def multi_level_inverse(pyr: Pyramid, wavelet, boundary="periodic", undo_scaling
     flat = _dev_f32(pyr.flat, "pyramid").contiguous()
     if flat.numel() != pyr.width * pyr.height:
         raise ValueError("pyramid detail plane size does not match its level")
-    out = torch.empty((pyr.height, pyr.width), device=flat.device, dtype=torch.float32)
-    scratch = torch.empty(max(lib().wl_pyramid_scratch_elems(pyr.width, pyr.height,
-                                                              pyr.levels), 1),
-                          device=flat.device, dtype=torch.float32)
+    if out is None:
+        out = torch.empty((pyr.height, pyr.width), device=flat.device, dtype=torch.float32)
+    need = lib().wl_pyramid_scratch_elems(pyr.width, pyr.height, pyr.levels)
+    if scratch is None or scratch.numel() < need:
+        scratch = torch.empty(max(need, 1), device=flat.device, dtype=torch.float32)
     _check(lib().wl_dwt2_pyramid_inverse(flat.data_ptr(), pyr.width, pyr.height, pyr.levels,
                                          w.index, kind, _index(BOUNDARIES, boundary, "boundary"),
                                          int(bool(undo_scaling)), out.data_ptr(),

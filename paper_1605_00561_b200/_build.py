@@ -17,7 +17,9 @@ CSRC = os.path.join(PKG, "csrc")
 # WL_VARIANT=<tag> with WL_DEFS="-DX=1 ..." builds an A/B variant library
 # (libwavelift_b200_<tag>.so) for tuning experiments; loaded via WL_LIB.
 VARIANT = os.environ.get("WL_VARIANT", "")
-OBJ = os.path.join(PKG, "_obj" + ("_" + VARIANT if VARIANT else ""))
+# variant objects live OUTSIDE the repo (they must not travel to the GPU box)
+OBJ = (os.path.join(os.environ.get("WL_OBJV", "/tmp/wl_objv"), VARIANT) if VARIANT
+       else os.path.join(PKG, "_obj"))
 LIB = os.path.join(PKG, "libwavelift_b200" + ("_" + VARIANT if VARIANT else "") + ".so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -26,7 +28,8 @@ FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
                 "-I" + os.path.join(ROOT, "include")] + os.environ.get("WL_DEFS", "").split()
 SOURCES = ["wl_capi.cu", "wl_interp.cu", "wl_fast.cu", "wl_fast_cdf53_fwd.cu",
            "wl_fast_cdf53_inv.cu", "wl_fast_cdf97_fwd.cu", "wl_fast_cdf97_inv.cu", "wl_fast_cdf53_fused.cu",
-           "wl_fast_cdf97_fused.cu", "wl_conv.cu", "wl_strips.cu", "wl_host.cu", "wl_desc.cu"]
+           "wl_fast_cdf97_fused.cu", "wl_conv.cu", "wl_strips.cu", "wl_host.cu", "wl_desc.cu",
+           "wl_fast_cdf53_direct.cu", "wl_fast_cdf97_direct.cu"]
 
 
 def _deps():

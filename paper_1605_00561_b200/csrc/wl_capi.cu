@@ -7,6 +7,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "../../include/wl_dwt.h"
 #include "wl_internal.h"
@@ -56,7 +57,7 @@ int launch_level(WlLevel L, cudaStream_t s) {
         e = (engine != 1 && L.wavelet <= 1) ? wl_launch_conv_fast(L, s) : wl_launch_conv(L, s);
         return cuda_status(e, "conv_kernel");
     }
-    if (engine == 2 && !wl_fast_supported(L))
+    if ((engine == 2 || engine == 3) && !wl_fast_supported(L))
         return fail(WL_EINVAL, "fast engine does not support this wavelet/scheme");
     if (engine != 1 && wl_fast_supported(L)) {
         e = wl_launch_fast(L, s);
@@ -106,6 +107,8 @@ int strip_halo(int wavelet, int direction) {
 }  // namespace
 
 void wl_count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+int wl_engine() { return g_engine.load(); }
 
 int wl_fail(int code, const char* msg) { return fail(code, msg); }
 
@@ -343,10 +346,14 @@ int wl_forward_strip_wait(const float* strip, int w, int rows, int halo_rows, lo
 }
 
 bool wl_strip_shape_ok(int w, int rows, int halo_rows, int wavelet, int scheme, int direction) {
-    if (w <= 0 || rows <= 0 || !valid_ids(wavelet, scheme, 0) || wavelet > WL_CDF97) return false;
+    return wl_strip_mode(w, rows, halo_rows, wavelet, scheme, direction) != 0;
+}
+
+int wl_strip_mode(int w, int rows, int halo_rows, int wavelet, int scheme, int direction) {
+    if (w <= 0 || rows <= 0 || !valid_ids(wavelet, scheme, 0) || wavelet > WL_CDF97) return 0;
     if (direction == 1 && scheme == WL_CONVOLUTION) scheme = WL_SWELDENS;
     const WlProgram& P = wl_host_program(prog_index(wavelet, scheme, direction));
-    if (P.is_conv) return w % 2 == 0 && rows % 2 == 0;  // the conv kernel takes any even shape
+    if (P.is_conv) return w % 2 == 0 && rows % 2 == 0 ? 3 : 0;  // any even shape
     // a level descriptor shaped like the strip call's, at dummy aligned addresses
     const float* dummy = reinterpret_cast<const float*>(static_cast<uintptr_t>(1) << 20);
     WlLevel L{};
@@ -375,7 +382,7 @@ bool wl_strip_shape_ok(int w, int rows, int halo_rows, int wavelet, int scheme, 
         L.ylo = halo_rows;
         L.yhi = halo_rows + rows;
     }
-    return wl_fast_supported(L);
+    return wl_fast_mode(L);
 }
 
 extern "C" {
@@ -446,9 +453,9 @@ int wl_dwt2_pyramid_forward(const float* img, int w, int h, int levels, int wave
 }
 
 // transform.cpp:229-256: coarsest level first.
-int wl_dwt2_pyramid_inverse(const float* pyramid, int w, int h, int levels, int wavelet,
-                            int scheme, int boundary, int undo_scaling, float* img,
-                            float* scratch, void* stream) {
+static int pyramid_inverse_impl(const float* pyramid, int w, int h, int levels, int wavelet,
+                                int scheme, int boundary, int undo_scaling, float* img,
+                                float* scratch, void* stream) {
     if (levels < 1) return fail(WL_EINVAL, "levels must be >= 1");
     const int div = 1 << (levels > 30 ? 30 : levels);
     if (w <= 0 || h <= 0 || levels > 30 || w % div != 0 || h % div != 0)
@@ -488,10 +495,10 @@ size_t wl_pyramid_batch_scratch_elems(int w, int h, int levels, int n) {
 // per level for the whole batch. Image b is at imgs + b*img_stride (pitch w),
 // its flat pyramid at pyramids + b*pyr_stride; level LL planes ping-pong in
 // `scratch` (wl_pyramid_batch_scratch_elems floats).
-int wl_dwt2_pyramid_forward_batch(const float* imgs, int w, int h, long img_stride, int n,
-                                  int levels, int wavelet, int scheme, int boundary, int scaling,
-                                  float* pyramids, long pyr_stride, float* scratch,
-                                  void* stream) {
+static int pyramid_forward_batch_impl(const float* imgs, int w, int h, long img_stride, int n,
+                                      int levels, int wavelet, int scheme, int boundary,
+                                      int scaling, float* pyramids, long pyr_stride,
+                                      float* scratch, void* stream) {
     if (n < 0) return fail(WL_EINVAL, "batch size must be >= 0");
     if (levels < 1) return fail(WL_EINVAL, "levels must be >= 1");
     if (w <= 0 || h <= 0) return fail(WL_EINVAL, "forward requires even positive dimensions");
@@ -596,10 +603,10 @@ int wl_dwt2_pyramid_forward_batch(const float* imgs, int w, int h, long img_stri
 }
 
 // Batched multi_level_inverse (transform.cpp:229-256 per image).
-int wl_dwt2_pyramid_inverse_batch(const float* pyramids, int w, int h, long pyr_stride, int n,
-                                  int levels, int wavelet, int scheme, int boundary,
-                                  int undo_scaling, float* imgs, long img_stride, float* scratch,
-                                  void* stream) {
+static int pyramid_inverse_batch_impl(const float* pyramids, int w, int h, long pyr_stride,
+                                      int n, int levels, int wavelet, int scheme, int boundary,
+                                      int undo_scaling, float* imgs, long img_stride,
+                                      float* scratch, void* stream) {
     if (n < 0) return fail(WL_EINVAL, "batch size must be >= 0");
     if (levels < 1) return fail(WL_EINVAL, "levels must be >= 1");
     if (w <= 0 || h <= 0 || levels > 30 || w % (1 << levels) != 0 || h % (1 << levels) != 0)
@@ -650,6 +657,174 @@ int wl_dwt2_pyramid_inverse_batch(const float* pyramids, int w, int h, long pyr_
         ll_stride = L.out_bstride[0];
     }
     return WL_OK;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------ graph cache
+// The multi-level drivers (transform.cpp:198-256) issue one launch (plus TMA
+// descriptor encodes) per level. A call repeated with identical arguments is
+// replayed from a CUDA graph: the first call runs eagerly (and warms every
+// lazy per-kernel setup), the second is captured on a thread-local stream
+// and instantiated, every later one is one cudaGraphLaunch on the caller's
+// stream. Any capture failure falls back to eager launches for that key.
+// WL_GRAPHS=0 (or wl_set_graphs(0)) disables it.
+namespace {
+
+std::atomic<int> g_graphs{[] {
+    const char* v = getenv("WL_GRAPHS");
+    return v && v[0] == '0' ? 0 : 1;
+}()};
+
+struct GraphKey {
+    int fn, device, engine, fuse;
+    int w, h, n, levels, wavelet, scheme, boundary, scaling;
+    const void *a, *b, *c;
+    long s1, s2;
+    bool operator==(const GraphKey& o) const { return std::memcmp(this, &o, sizeof o) == 0; }
+};
+
+struct GraphEntry {
+    GraphKey key;
+    cudaGraphExec_t exec = nullptr;
+    long kernels = 0;  // kernel nodes (added to wl_launch_count per replay)
+    int state = 0;     // 0 seen once, 1 captured, 2 eager only
+    unsigned long long used = 0;
+};
+
+struct GraphCache {
+    static constexpr int kMax = 16;
+    GraphEntry e[kMax];
+    int n = 0;
+    unsigned long long tick = 0;
+    cudaStream_t cap[64] = {};
+    ~GraphCache() {
+        for (int i = 0; i < n; ++i)
+            if (e[i].exec) cudaGraphExecDestroy(e[i].exec);
+    }
+    GraphEntry* find(const GraphKey& k) {
+        for (int i = 0; i < n; ++i)
+            if (e[i].key == k) return &e[i];
+        return nullptr;
+    }
+    GraphEntry* insert(const GraphKey& k) {
+        int slot = n < kMax ? n++ : 0;
+        if (slot == 0 && n == kMax)
+            for (int i = 1; i < kMax; ++i)
+                if (e[i].used < e[slot].used) slot = i;
+        if (e[slot].exec) cudaGraphExecDestroy(e[slot].exec);
+        e[slot] = GraphEntry{};
+        e[slot].key = k;
+        return &e[slot];
+    }
+};
+
+thread_local GraphCache g_cache;
+
+template <class F>
+int with_graph(GraphKey k, void* stream, F&& run) {
+    if (!g_graphs.load()) return run(stream);
+    cudaGetDevice(&k.device);
+    k.engine = g_engine.load();
+    k.fuse = g_fuse.load();
+    GraphCache& c = g_cache;
+    GraphEntry* e = c.find(k);
+    if (!e) {
+        e = c.insert(k);
+        e->used = ++c.tick;
+        return run(stream);  // first call: eager
+    }
+    e->used = ++c.tick;
+    if (e->state == 2) return run(stream);
+    if (e->state == 0) {
+        cudaStream_t& cs = c.cap[k.device & 63];
+        if (!cs && cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess) {
+            cs = nullptr;
+            e->state = 2;
+            cudaGetLastError();
+            return run(stream);
+        }
+        const long before = g_launches.load();
+        cudaGraph_t g = nullptr;
+        int st = WL_ERUNTIME;
+        if (cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
+            st = run(cs);
+            if (cudaStreamEndCapture(cs, &g) != cudaSuccess) st = WL_ERUNTIME;
+        }
+        g_launches.store(before);  // captured, not launched
+        if (st == WL_OK && g && cudaGraphInstantiate(&e->exec, g, 0) == cudaSuccess) {
+            size_t nn = 0;
+            cudaGraphGetNodes(g, nullptr, &nn);
+            std::vector<cudaGraphNode_t> nodes(nn);
+            if (nn) cudaGraphGetNodes(g, nodes.data(), &nn);
+            for (cudaGraphNode_t nd : nodes) {
+                cudaGraphNodeType t;
+                if (cudaGraphNodeGetType(nd, &t) == cudaSuccess && t == cudaGraphNodeTypeKernel)
+                    ++e->kernels;
+            }
+            e->state = 1;
+        } else {
+            e->exec = nullptr;
+            e->state = 2;
+        }
+        if (g) cudaGraphDestroy(g);
+        cudaGetLastError();  // clear capture-related errors; eager path reports its own
+        if (e->state == 2) return run(stream);
+    }
+    const cudaError_t le = cudaGraphLaunch(e->exec, static_cast<cudaStream_t>(stream));
+    if (le != cudaSuccess) return cuda_status(le, "cudaGraphLaunch");
+    g_launches.fetch_add(e->kernels);
+    return WL_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int wl_set_graphs(int on) { return g_graphs.exchange(on ? 1 : 0); }
+
+int wl_dwt2_pyramid_forward_batch(const float* imgs, int w, int h, long img_stride, int n,
+                                  int levels, int wavelet, int scheme, int boundary, int scaling,
+                                  float* pyramids, long pyr_stride, float* scratch,
+                                  void* stream) {
+    GraphKey k{};
+    k.fn = 1;
+    k.w = w; k.h = h; k.n = n; k.levels = levels; k.wavelet = wavelet; k.scheme = scheme;
+    k.boundary = boundary; k.scaling = scaling;
+    k.a = imgs; k.b = pyramids; k.c = scratch; k.s1 = img_stride; k.s2 = pyr_stride;
+    return with_graph(k, stream, [&](void* st) {
+        return pyramid_forward_batch_impl(imgs, w, h, img_stride, n, levels, wavelet, scheme,
+                                          boundary, scaling, pyramids, pyr_stride, scratch, st);
+    });
+}
+
+int wl_dwt2_pyramid_inverse_batch(const float* pyramids, int w, int h, long pyr_stride, int n,
+                                  int levels, int wavelet, int scheme, int boundary,
+                                  int undo_scaling, float* imgs, long img_stride, float* scratch,
+                                  void* stream) {
+    GraphKey k{};
+    k.fn = 2;
+    k.w = w; k.h = h; k.n = n; k.levels = levels; k.wavelet = wavelet; k.scheme = scheme;
+    k.boundary = boundary; k.scaling = undo_scaling;
+    k.a = pyramids; k.b = imgs; k.c = scratch; k.s1 = pyr_stride; k.s2 = img_stride;
+    return with_graph(k, stream, [&](void* st) {
+        return pyramid_inverse_batch_impl(pyramids, w, h, pyr_stride, n, levels, wavelet, scheme,
+                                          boundary, undo_scaling, imgs, img_stride, scratch, st);
+    });
+}
+
+int wl_dwt2_pyramid_inverse(const float* pyramid, int w, int h, int levels, int wavelet,
+                            int scheme, int boundary, int undo_scaling, float* img,
+                            float* scratch, void* stream) {
+    GraphKey k{};
+    k.fn = 3;
+    k.w = w; k.h = h; k.n = 1; k.levels = levels; k.wavelet = wavelet; k.scheme = scheme;
+    k.boundary = boundary; k.scaling = undo_scaling;
+    k.a = pyramid; k.b = img; k.c = scratch;
+    return with_graph(k, stream, [&](void* st) {
+        return pyramid_inverse_impl(pyramid, w, h, levels, wavelet, scheme, boundary,
+                                    undo_scaling, img, scratch, st);
+    });
 }
 
 }  // extern "C"

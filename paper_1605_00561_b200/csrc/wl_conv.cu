@@ -21,6 +21,11 @@ namespace {
 #ifndef WL_CONV_Q
 #define WL_CONV_Q 4
 #endif
+// Row segments via lane-swizzled 16-byte loads + shuffles (1) or overlapping
+// 8-byte loads (0: 4-way shared-memory bank conflicts)
+#ifndef WL_CONV_SHFL
+#define WL_CONV_SHFL 1
+#endif
 #ifndef WL_CONV_TQY
 #define WL_CONV_TQY 32
 #endif
@@ -107,6 +112,40 @@ __global__ void __launch_bounds__(NT) conv_fast_kernel(const __grid_constant__ C
         for (int q = 0; q < Q; ++q)
 #pragma unroll
             for (int c = 0; c < 4; ++c) acc[q][c] = 0.f;
+#if WL_CONV_SHFL
+        // Row segment of the lane's Q quads: its own 2Q pixels with two
+        // 16-byte loads in a lane-swizzled order (every 8-lane phase covers
+        // all 32 banks: conflict-free), the -kCol0 / kCol1 halo pixels from
+        // the neighbour lanes by shuffle (a half-warp spans one 64-quad tile
+        // row); only the segment's edge lanes read their halo from memory.
+        static_assert(Q == 4 && TQX == 64, "shuffle layout: 16 lanes x 4 quads per row");
+        constexpr int HL = -C::kCol0, HR = C::kCol1;
+        const int lane = threadIdx.x & 31, sw = (lane >> 2) & 1;
+        wlfast::sfor<C::kRow1 - C::kRow0 + 1>([&](auto y_) {
+            constexpr int Y = decltype(y_)::value + C::kRow0;
+            const float* own = px + (2 * qr + Y - C::kRow0) * SW + MARGIN + 2 * Q * qb;
+            const float4 u0 = *reinterpret_cast<const float4*>(own + 4 * sw);
+            const float4 u1 = *reinterpret_cast<const float4*>(own + 4 * (sw ^ 1));
+            const float4 lo = sw ? u1 : u0, hi = sw ? u0 : u1;
+            const float o[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+            float seg[G::kSeg];
+#pragma unroll
+            for (int i = 0; i < HL; ++i) seg[i] = __shfl_up_sync(0xffffffffu, o[8 - HL + i], 1, 16);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) seg[HL + i] = o[i];
+#pragma unroll
+            for (int i = 0; i < HR; ++i) seg[HL + 8 + i] = __shfl_down_sync(0xffffffffu, o[i], 1, 16);
+            if (qb == 0) {
+#pragma unroll
+                for (int i = 0; i < HL; ++i) seg[i] = own[i - HL];
+            }
+            if (qb == kBlocksX - 1) {
+#pragma unroll
+                for (int i = 0; i < HR; ++i) seg[HL + 8 + i] = own[8 + i];
+            }
+            C::template row<Y, Q>(seg, acc);
+        });
+#else
         // pixel column of seg[0] inside the staged tile
         const int sx = 2 * Q * qb + MARGIN + C::kCol0;
         wlfast::sfor<C::kRow1 - C::kRow0 + 1>([&](auto y_) {
@@ -121,6 +160,7 @@ __global__ void __launch_bounds__(NT) conv_fast_kernel(const __grid_constant__ C
             }
             C::template row<Y, Q>(seg, acc);
         });
+#endif
         const int gy = r0 + qr, gx = c0 + Q * qb;
         if (gy >= a.yhi) continue;
         if (a.scaling) {

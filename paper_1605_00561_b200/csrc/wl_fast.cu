@@ -50,6 +50,10 @@ cudaError_t wl_fast_cdf97_fwd(int scheme, const WlLevel& L, const wlfast::Plan& 
                               cudaStream_t s);
 cudaError_t wl_fast_cdf97_inv(int scheme, const WlLevel& L, const wlfast::Plan& p,
                               cudaStream_t s);
+cudaError_t wl_fast_cdf53_direct(int scheme, const WlLevel& L, const wlfast::Plan& p,
+                                 cudaStream_t s);
+cudaError_t wl_fast_cdf97_direct(int scheme, const WlLevel& L, const wlfast::Plan& p,
+                                 cudaStream_t s);
 cudaError_t wl_fast_cdf53_fwd_fused(int scheme, const WlLevel& L0, const wlfast::Plan& p0,
                                    const WlLevel& L1, const wlfast::Plan& p1, unsigned* ctr,
                                    cudaStream_t s);
@@ -95,8 +99,12 @@ bool aligned(const void* p, int bytes) { return (reinterpret_cast<uintptr_t>(p) 
 
 }  // namespace
 
-bool wl_fast_supported(const WlLevel& L) {
-    if (L.wavelet < 0 || L.wavelet > 1 || L.scheme < 0 || L.scheme > 8) return false;
+namespace {
+
+// The TMA path: 16-byte aligned boxes and pitches (tensor maps), and for
+// CPT = 4 the aligned float4 stores (plane widths and pitches in multiples
+// of 4 cells).
+bool tma_ok(const WlLevel& L, int CPT) {
     if (!wlfast::encode_fn()) return false;
     if (L.direction == 0) {
         if (!aligned(L.in[0], 16) || (L.in_pitch % 4) != 0) return false;
@@ -112,27 +120,55 @@ bool wl_fast_supported(const WlLevel& L) {
     if (L.nb > 1)
         for (int k = 0; k < 4; ++k)
             if ((L.in_bstride[k] % 4) != 0 || (L.out_bstride[k] % 4) != 0) return false;
-    int R, NW, CPT;
-    geometry(L, &R, &NW, &CPT);
-    // CPT = 4 stores aligned float4 groups: plane widths and pitches in
-    // multiples of 4 cells, 16-byte aligned outputs
     if (CPT == 4) {
         if (L.qw % 4 != 0 || L.out_pitch % 4 != 0) return false;
         for (int k = 0; k < (L.direction == 0 ? 4 : 1); ++k)
             if (!aligned(L.out[k], 16) || (L.nb > 1 && L.out_bstride[k] % 4 != 0)) return false;
     }
-    const int H = wl_host_program(L.prog).halo;
-    return wlfast::plan_tiles(L, H, R, NW, CPT).ok;
+    return true;
 }
 
-cudaError_t wl_launch_fast(const WlLevel& L, cudaStream_t stream) {
-    if (!wl_fast_supported(L)) return cudaErrorNotSupported;
+// The direct-load path: float2 loads of pixel pairs (forward), scalar
+// everything else; no halo wait (the strip runtime then waits in its
+// exchange kernel).
+bool direct_ok(const WlLevel& L) {
+    if (L.xflag_a) return false;
+    if (L.direction == 0) {
+        if (!aligned(L.in[0], 8)) return false;
+        if (L.nb > 1 && L.in_bstride[0] % 2 != 0) return false;
+    }
+    for (int k = 0; k < 4; ++k)
+        if ((L.in[k] && !aligned(L.in[k], 4)) || (L.out[k] && !aligned(L.out[k], 4))) return false;
+    return true;
+}
+
+}  // namespace
+
+int wl_fast_mode(const WlLevel& L) {
+    if (L.wavelet < 0 || L.wavelet > 1 || L.scheme < 0 || L.scheme > 8) return 0;
     int R, NW, CPT;
     geometry(L, &R, &NW, &CPT);
     const int H = wl_host_program(L.prog).halo;
-    const wlfast::Plan plan = wlfast::plan_tiles(L, H, R, NW, CPT);
+    const bool force_direct = wl_engine() == 3;
+    if (!force_direct && tma_ok(L, CPT) && wlfast::plan_tiles(L, H, R, NW, CPT).ok) return 1;
+    if (direct_ok(L) && wlfast::plan_tiles(L, H, R, NW, CPT, true).ok) return 2;
+    return 0;
+}
+
+bool wl_fast_supported(const WlLevel& L) { return wl_fast_mode(L) != 0; }
+
+cudaError_t wl_launch_fast(const WlLevel& L, cudaStream_t stream) {
+    const int mode = wl_fast_mode(L);
+    if (!mode) return cudaErrorNotSupported;
+    int R, NW, CPT;
+    geometry(L, &R, &NW, &CPT);
+    const int H = wl_host_program(L.prog).halo;
+    const wlfast::Plan plan = wlfast::plan_tiles(L, H, R, NW, CPT, mode == 2);
     cudaError_t e;
-    if (L.wavelet == 0)
+    if (mode == 2)
+        e = L.wavelet == 0 ? wl_fast_cdf53_direct(L.scheme, L, plan, stream)
+                           : wl_fast_cdf97_direct(L.scheme, L, plan, stream);
+    else if (L.wavelet == 0)
         e = L.direction == 0 ? wl_fast_cdf53_fwd(L.scheme, L, plan, stream)
                              : wl_fast_cdf53_inv(L.scheme, L, plan, stream);
     else
@@ -180,7 +216,7 @@ cudaError_t wl_launch_fast_fused(const WlLevel& L0, const WlLevel& L1, unsigned*
         L1.in_pitch != L0.out_pitch || (L0.nb > 1 && L1.in_bstride[0] != L0.out_bstride[0]))
         return cudaErrorNotSupported;
     if (wl_host_program(L0.prog).is_conv) return cudaErrorNotSupported;
-    if (!wl_fast_supported(L0) || !wl_fast_supported(L1)) return cudaErrorNotSupported;
+    if (wl_fast_mode(L0) != 1 || wl_fast_mode(L1) != 1) return cudaErrorNotSupported;
     int R, NW, CPT;
     geometry(L0, &R, &NW, &CPT);
     const int H = wl_host_program(L0.prog).halo;

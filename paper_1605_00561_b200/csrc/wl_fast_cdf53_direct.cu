@@ -1,0 +1,28 @@
+// Instantiation unit of the fast engine: cdf53, direct-load variant (no TMA;
+// wlfast::launch_direct), both directions, all lifting schemes.
+#include "wl_fast_impl.cuh"
+
+cudaError_t wl_fast_cdf53_direct(int scheme, const WlLevel& L, const wlfast::Plan& p,
+                               cudaStream_t s) {
+#define WL_CASE(wi, si, d, P)                                                               \
+    case si:                                                                                \
+        return wlfast::launch_direct<P, d, wlfast::SchemeConfig<wi, d, si>::R,              \
+                                     wlfast::SchemeConfig<wi, d, si>::NW,                   \
+                                     wlfast::SchemeConfig<wi, d, si>::CPT,                  \
+                                     wlfast::SchemeConfig<wi, d, si>::NS,                   \
+                                     wlfast::SchemeConfig<wi, d, si>::XF,                   \
+                                     wlfast::SchemeConfig<wi, d, si>::MAXB>(L, p, s);
+    if (L.direction == 0) {
+        switch (scheme) {
+            WL_FAST_FOREACH_0_0(WL_CASE)
+            default:
+                return cudaErrorNotSupported;
+        }
+    }
+    switch (scheme) {
+        WL_FAST_FOREACH_0_1(WL_CASE)
+        default:
+            return cudaErrorNotSupported;
+    }
+#undef WL_CASE
+}

@@ -465,14 +465,21 @@ constexpr int xch_comps() {
     return mx;
 }
 
+// DIRECT: no TMA -- shapes whose pitches/pointers/widths the TMA boxes and
+// the aligned float4 stores cannot take (e.g. 8190^2 images: 32760-byte rows,
+// odd plane widths). Every tile loads its cells with coalesced per-lane
+// global loads (the periodic border-tile path) and stores element by element
+// under a column mask; the producer warp exits at once and the stage ring is
+// not allocated. Same instruction sequence per cell, so the same results.
 template <class P, int DIR, int R, int NW, int CPT, int NS, bool XF, bool MIRROR,
-          bool FUSED = false>
+          bool FUSED = false, bool DIRECT = false>
 __global__ void __launch_bounds__((NW + 1) * 32,
                                   (Geometry<R, NW, CPT, NS, xch_comps<P, XF>()>::kMinBlocks))
     fast_kernel(const __grid_constant__ CUtensorMap m0, const __grid_constant__ CUtensorMap m1,
                 const __grid_constant__ CUtensorMap m2, const __grid_constant__ CUtensorMap m3,
                 const __grid_constant__ KArgs K) {
     static_assert(!FUSED || (DIR == 0 && !MIRROR), "fused launches: periodic forwards");
+    static_assert(!DIRECT || (!FUSED && !MIRROR), "direct-load launches: plain plans");
     __shared__ int4 task_sm[NS];  // fused: the task of each stage (producer -> consumers)
     // fused: per processed tile (ring of kRing), warps done storing / its level-l row
     constexpr int kRing = 8;
@@ -486,7 +493,7 @@ __global__ void __launch_bounds__((NW + 1) * 32,
     constexpr int HX = halo_x<CPT, H>();
     extern __shared__ __align__(128) unsigned char smem_raw[];
     float* stage = reinterpret_cast<float*>(smem_raw);
-    float* xch = stage + NS * G::kStageFloats;
+    float* xch = stage + (DIRECT ? 0 : NS * G::kStageFloats);
     uint64_t* full = reinterpret_cast<uint64_t*>(xch + G::kXchFloats);
     uint64_t* empty = full + NS;
 
@@ -509,6 +516,7 @@ __global__ void __launch_bounds__((NW + 1) * 32,
 
     if (warp == NW) {
         // ---------------- producer warp: TMA tile stream ----------------
+        if constexpr (DIRECT) return;  // compute warps load their own cells
         if (FUSED && lane == 0) {
             const FuseArgs& f = K.fu;
             // Level-l tasks are claimed in chunks of kClaim, the next chunk one
@@ -764,13 +772,15 @@ __global__ void __launch_bounds__((NW + 1) * 32,
             if (a.filter && border != (a.filter == 2)) return;  // the other launch's tile
             const unsigned phase = (i / NS) & 1;  // fill count of stage s (processed tiles)
             ++i;
-            const bool wrap_tile = a.wrap && border;
+            // DIRECT: every tile loads from global memory (coordinates wrapped,
+            // which is the identity inside the image)
+            const bool wrap_tile = DIRECT || (a.wrap && border);
             // Symmetric border tile: out-of-image cells come zero-filled from the
             // TMA box and are never read as such -- before every neighbour step
             // the distance-1 ghosts are overwritten with their mirror images.
             const bool mtile = MIRROR && a.mirror && border;
             const int gy0m = cy + 1 + warp * R;  // image row of v[0]
-            if constexpr (!FUSED) mbar_wait(&full[s], phase);
+            if constexpr (!FUSED && !DIRECT) mbar_wait(&full[s], phase);
             const float* st = stage + s * G::kStageFloats;
 
             // Load the warp's rows (+ one ghost row above and below) and split
@@ -867,8 +877,10 @@ __global__ void __launch_bounds__((NW + 1) * 32,
             // let the next TMA overwrite rows other lanes had not finished
             // reading), and the proxy fence orders these generic-proxy reads
             // before the async-proxy (TMA) writes of the refill.
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            mbar_arrive(&empty[s]);
+            if constexpr (!DIRECT) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                mbar_arrive(&empty[s]);
+            }
 
             if (DIR == 1 && a.scaling) {  // undo scaling first (transform.cpp:180)
 #pragma unroll
@@ -1081,7 +1093,33 @@ __global__ void __launch_bounds__((NW + 1) * 32,
 #pragma unroll
             for (int k = 0; k < (DIR == 0 ? 4 : 1); ++k) pk[k] = a.out[k] + b * a.out_bstride[k] + off0;
             const long step = DIR == 0 ? a.out_pitch : 2 * a.out_pitch;
-            if constexpr (CPT == 4) {
+            if constexpr (DIRECT) {
+                // element-wise stores under a per-cell column mask (any pitch,
+                // any plane width); row validity is warp-uniform
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const int qr = warp * R + r;
+                    const int gy = gy0 + r;
+                    const bool row_ok = qr >= H && qr < H + a.TH && gy >= a.ylo && gy < a.yhi;
+#pragma unroll
+                    for (int j = 0; j < CPT; ++j) {
+                        const int cl = CPT * lane + j;  // cell column inside the compute region
+                        const bool ok = row_ok && cl >= HX && cl < HX + a.TW && gx + j >= 0 &&
+                                        gx + j < a.qw;
+                        if (!ok) continue;
+                        if (DIR == 0) {
+#pragma unroll
+                            for (int k = 0; k < 4; ++k) pk[k][r * step + j] = v[r][j][k];
+                        } else {
+                            float* p0 = pk[0] + r * step + 2 * j;
+                            p0[0] = v[r][j][0];
+                            p0[1] = v[r][j][1];
+                            p0[a.out_pitch] = v[r][j][2];
+                            p0[a.out_pitch + 1] = v[r][j][3];
+                        }
+                    }
+                }
+            } else if constexpr (CPT == 4) {
                 // Whole-lane halo (lanes 0 and 31): a lane stores its 4 cells as
                 // one aligned float4 per plane (qw = 0 mod 4, cx = 0 mod 4), or
                 // nothing. Row validity is warp-uniform.
@@ -1365,7 +1403,7 @@ struct Plan {
 //    [ylo, yhi) only; the rows around them are halo rows physically present
 //    in the buffer (ylo >= H + 1 and yhi <= qh - H - 1 keep every stored
 //    cell's dependency cone and the tiles' ghost rows inside the buffer).
-inline Plan plan_tiles(const WlLevel& L, int H, int R, int NW, int CPT) {
+inline Plan plan_tiles(const WlLevel& L, int H, int R, int NW, int CPT, bool no_mirror = false) {
     Plan p{};
     const int nb = L.nb > 1 ? L.nb : 1;
     p.args.ylo = 0;
@@ -1387,7 +1425,7 @@ inline Plan plan_tiles(const WlLevel& L, int H, int R, int NW, int CPT) {
     // (kernel `mtile`); otherwise only interior tiles run here and the frame
     // goes to the interpreter.
     bool full_sym = L.boundary == 1 && L.yhi == 0 && L.qw >= 2 && L.qh >= 2 &&
-                    L.qw % CPT == 0 && WL_SYM_FAST;
+                    L.qw % CPT == 0 && WL_SYM_FAST && !no_mirror;
     // Row offset of the symmetric grid: every tile whose compute rows hold
     // image row 0 must not have it as a warp's last row (its mirror source,
     // row 1, would sit in the next warp), nor row qh-1 as a warp's first row.
@@ -1536,6 +1574,51 @@ cudaError_t launch(const WlLevel& L, const Plan& plan, cudaStream_t stream) {
     cudaError_t e = run(fast_kernel<P, DIR, R, NW, CPT, NS, XF, false>, cap_norm, 1);
     if (e != cudaSuccess) return e;
     return run(fast_kernel<P, DIR, R, NW, CPT, NS, XF, true>, cap_mirr, 2);
+}
+
+// Direct-load launch (no TMA, element-wise stores): shapes the TMA path
+// cannot take. Plain plans only (periodic whole image, strip windows, or the
+// symmetric interior grid + interpreter frame).
+template <class P, int DIR, int R, int NW, int CPT, int NS, bool XF, int MAXB>
+cudaError_t launch_direct(const WlLevel& L, const Plan& plan, cudaStream_t stream) {
+    constexpr int NXC = xch_comps<P, XF>();
+    using G = Geometry<R, NW, CPT, NS, NXC>;
+    if (plan.args.mirror) return cudaErrorNotSupported;
+    KArgs k{};
+    FastArgs& a = k.lv[0];
+    a = plan.args;
+    const int nb = L.nb > 1 ? L.nb : 1;
+    for (int q = 0; q < 4; ++q) {
+        a.in[q] = L.in[q];
+        a.out[q] = DIR == 0 ? L.out[q] : (q == 0 ? L.out[0] : nullptr);
+        a.in_bstride[q] = nb > 1 ? L.in_bstride[q] : 0;
+        a.out_bstride[q] = nb > 1 ? L.out_bstride[q] : 0;
+    }
+    a.xflag_a = a.xflag_b = nullptr;
+    a.in_pitch = L.in_pitch;
+    a.out_pitch = L.out_pitch;
+    a.scaling = L.scaling && wl_host_program(L.prog).has_scale;
+    a.scale = wl_host_program(L.prog).scale;
+    a.filter = 0;
+    constexpr size_t smem = (size_t)G::kXchFloats * 4 + 16 * NS;
+    auto kern = fast_kernel<P, DIR, R, NW, CPT, NS, XF, false, false, true>;
+    static int cap[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int& mb = cap[dev & 63];
+    if (mb == 0) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        int per_sm = 0, sms = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (NW + 1) * 32, smem);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        mb = (per_sm > 0 ? per_sm : 1) * sms;
+    }
+    const int grid = a.ntiles < mb ? a.ntiles : mb;
+    CUtensorMap none{};
+    cudaError_t le = launch_pdl(kern, dim3(grid), dim3((NW + 1) * 32), smem, stream, none, none,
+                                none, none, k);
+    wl_count_launch();
+    return le != cudaSuccess ? le : cudaGetLastError();
 }
 
 // Fused launch of two consecutive periodic forward levels (L1 reads L0's LL

@@ -58,6 +58,11 @@ cudaError_t wl_launch_conv_fast(const WlLevel& L, cudaStream_t stream);
 // (wavelet, scheme, direction) has no fast instantiation.
 cudaError_t wl_launch_fast(const WlLevel& L, cudaStream_t stream);
 bool wl_fast_supported(const WlLevel& L);
+// 0 = no fast instantiation, 1 = TMA path, 2 = direct-load path (no TMA:
+// unaligned pitches/pointers, plane widths not = 0 mod 4 cells).
+int wl_fast_mode(const WlLevel& L);
+// wl_set_engine's value (0 auto, 1 interpreter, 2 fast, 3 fast direct-load).
+int wl_engine();
 // Two consecutive periodic forward pyramid levels (L1 reads L0's LL) in one
 // persistent launch; cudaErrorNotSupported when the pair does not qualify
 // (then launch them one by one). `ctr`: wl_fused_ctr_elems(L0.qh, nb) words.
@@ -82,3 +87,6 @@ int wl_forward_strip_wait(const float* strip, int w, int rows, int halo_rows, lo
 // and below); inverse (direction 1): w = plane cells, rows = plane rows.
 // Asked by the host chunk pipeline and WlStrips BEFORE anything is enqueued.
 bool wl_strip_shape_ok(int w, int rows, int halo_rows, int wavelet, int scheme, int direction);
+// ... and how: 0 unsupported, 1 fast engine with TMA (halo wait foldable into
+// the transform), 2 fast engine direct-load path, 3 convolution kernel.
+int wl_strip_mode(int w, int rows, int halo_rows, int wavelet, int scheme, int direction);

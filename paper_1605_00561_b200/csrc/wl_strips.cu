@@ -195,14 +195,12 @@ int wl_strips_create(int w, int h, int rank, int nranks, int levels, int wavelet
     const int halo = wl_strip_halo_rows(wavelet, scheme, 0);
     if ((rows >> (levels - 1)) < halo)
         return sfail(WL_EINVAL, "strip too thin for the halo at the deepest level");
-    if (((w >> (levels - 1)) * 4) % 16 != 0)
-        return sfail(WL_EINVAL, "level widths must keep 16-byte aligned rows");
     // every level's strip transform must accept its shape: checked here, before
     // any exchange kernel or flag signal of a forward call is enqueued
     for (int l = 0; l < levels; ++l)
         if (!wl_strip_shape_ok(w >> l, rows >> l, halo, wavelet, scheme, 0))
-            return sfail(WL_EINVAL, "a pyramid level's width is not supported by the strip "
-                                    "kernels (lifting schemes need level widths = 0 mod 8)");
+            return sfail(WL_EINVAL, "a pyramid level's shape is not supported by the strip "
+                                    "kernels");
     WlStrips* s = new (std::nothrow) WlStrips();
     if (!s) return sfail(WL_ERUNTIME, "out of host memory");
     s->w = w;
@@ -406,7 +404,9 @@ int wl_strips_forward(WlStrips* s, float* slice, void* stream) {
         a.counter = my + 2 * L + 2;
         a.err = s->err_dev;
         a.vec4 = (wl_ % 4) == 0;
-        a.wait = overlap ? 0 : 1;
+        // the halo wait folds into the transform only on its TMA path
+        const bool ov = overlap && wl_strip_mode(wl_, sl_, halo, s->wavelet, s->scheme, 0) == 1;
+        a.wait = ov ? 0 : 1;
         const long work = a.vec4 ? a.n / 4 : a.n;
         int blocks = static_cast<int>((work + 255) / 256);
         blocks = blocks < 1 ? 1 : (blocks > 148 ? 148 : blocks);
@@ -424,8 +424,8 @@ int wl_strips_forward(WlStrips* s, float* slice, void* stream) {
                                  : s->lvl(s->window, l + 1) + static_cast<size_t>(halo) * qw;
         const int r = wl_forward_strip_wait(
             interior, wl_, sl_, halo, wl_, s->wavelet, s->scheme, s->scaling, ll, hl, hl + np,
-            hl + 2 * np, qw, stream, overlap ? my + 2 * l : nullptr,
-            overlap ? my + 2 * l + 1 : nullptr, e, s->err_dev);
+            hl + 2 * np, qw, stream, ov ? my + 2 * l : nullptr, ov ? my + 2 * l + 1 : nullptr, e,
+            s->err_dev);
         if (r != WL_OK) return r;
     }
     signal_kernel<<<1, 1, 0, st>>>(fu + 2 * L + 1, fd + 2 * L, e);

@@ -199,10 +199,21 @@ def test_strip_pyramid_errors(wl):
         wl.StripPyramid(256, 64, 4, sch, 0, 2)  # deepest strip thinner than the halo
     with pytest.raises(ValueError):
         wl.StripPyramid(256, 256, 2, wl.build_scheme("sweldens", "dd137"), 0, 1)
-    # level widths 1200, 600, 300: the deepest level (300 = 4 mod 8 px) has no
-    # strip kernel -- rejected at create, before any exchange is enqueued
-    with pytest.raises(ValueError):
-        wl.StripPyramid(1200, 1024, 3, sch, 0, 2)
+    with pytest.raises(ValueError):  # width not divisible by 2^levels
+        wl.StripPyramid(1100, 1024, 3, sch, 0, 2)
+
+
+@pytest.mark.parametrize("wavelet", ["cdf53", "cdf97"])
+def test_strip_pyramid_unaligned_levels(wl, wavelet):
+    """Level widths 1160, 580, 290 px (= 0, 4, 2 mod 8): the deeper levels run
+    the direct-load strip kernels (no TMA, halo wait in the exchange kernel);
+    still bit-identical to the whole-image pyramid."""
+    import torch
+    img = rand((512, 1160), 22)
+    sch = wl.build_scheme("monolithic_star", wavelet)
+    want = wl.multi_level_forward(img, sch, 3).flat
+    for n in (1, 2, 4):
+        assert torch.equal(_virtual_ranks(wl, img, 3, sch, n), want), n
 
 
 def _ipc_worker(rank, n, port, out_path):
