@@ -189,11 +189,25 @@ const char* wl_strips_last_error(void);
 size_t wl_strips_blob_bytes(void);
 int wl_strips_create(int w, int h, int rank, int nranks, int levels, int wavelet, int scheme,
                      int scaling, WlStrips** out);
+/* ... with a boundary: WL_SYMMETRIC strips are not a ring -- rank 0 and rank
+ * nranks-1 sit on the image's top / bottom edge (per-step mirroring there,
+ * transform.cpp:59-72); lifting schemes only. wl_strips_create is
+ * WL_PERIODIC. */
+int wl_strips_create_ex(int w, int h, int rank, int nranks, int levels, int wavelet, int scheme,
+                        int boundary, int scaling, WlStrips** out);
 int wl_strips_export(WlStrips* s, void* blob);
 int wl_strips_connect(WlStrips* s, const void* up_blob, const void* down_blob);
 float* wl_strips_input(WlStrips* s);
 size_t wl_strips_slice_elems(const WlStrips* s);
 int wl_strips_forward(WlStrips* s, float* slice, void* stream);
+/* multi_level_inverse (transform.cpp:229-256) of the rank's slice (the
+ * layout wl_strips_forward writes; `undo_scaling` = the create's scaling):
+ * writes the rank's rows x w rows of the reconstructed image (pitch w).
+ * Coarsest level first; per level `wl_strip_halo_rows(.., 1)` plane rows of
+ * all 4 planes are pushed to each neighbour over peer memory. Every rank
+ * calls it the same number of times, in the same order as forward. The
+ * scheme selects the inverse kernel (Convolution: the Sweldens inverse). */
+int wl_strips_inverse(WlStrips* s, const float* slice, float* out_rows, void* stream);
 /* WL_ERUNTIME if a halo wait timed out (call after synchronising). */
 int wl_strips_check(WlStrips* s);
 int wl_strips_destroy(WlStrips* s);

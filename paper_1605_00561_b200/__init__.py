@@ -75,6 +75,8 @@ def lib() -> ctypes.CDLL:
         l.wl_strips_slice_elems.restype = ctypes.c_size_t
         l.wl_strips_slice_elems.argtypes = [vp]
         l.wl_strips_forward.argtypes = [vp, fp, vp]
+        l.wl_strips_create_ex.argtypes = [i, i, i, i, i, i, i, i, i, ctypes.POINTER(vp)]
+        l.wl_strips_inverse.argtypes = [vp, fp, fp, vp]
         l.wl_strips_check.argtypes = [vp]
         l.wl_strips_destroy.argtypes = [vp]
         l.wl_dwt2_forward_host.argtypes = [fp, i, i, lg, i, i, i, i, fp, fp, fp, fp, lg]
@@ -636,20 +638,23 @@ class StripPyramid:
     """One rank's share of a row-strip multi-level pyramid (configs[3]).
 
     Rank `rank` of `nranks` owns image rows [rank*h/nranks, (rank+1)*h/nranks)
-    of an h x w image (periodic boundary). Levels exchange halo rows with the
-    neighbour ranks through peer memory (CUDA IPC), see include/wl_dwt.h.
+    of an h x w image (periodic: a ring; symmetric: ranks 0 and nranks-1 sit
+    on the image edges). Levels exchange halo rows with the neighbour ranks
+    through peer memory (CUDA IPC), see include/wl_dwt.h.
     Usage: `export()` -> share blobs -> `connect(up, down)` -> write
-    `input` -> `forward()` (collective: every rank calls it equally often)."""
+    `input` -> `forward()` / `inverse(slice)` (collective: every rank calls
+    them equally often, in the same order)."""
 
-    def __init__(self, w, h, levels, scheme: Scheme, rank=0, nranks=1, apply_scaling=False):
+    def __init__(self, w, h, levels, scheme: Scheme, rank=0, nranks=1, apply_scaling=False,
+                 boundary="periodic"):
         self.w, self.h, self.levels = w, h, levels
         self.rank, self.nranks = rank, nranks
         self.rows = h // nranks if nranks > 0 else 0
         self.scheme = scheme
         self._ctx = ctypes.c_void_p()
-        _scheck(lib().wl_strips_create(w, h, rank, nranks, levels, scheme.wavelet.index,
-                                       scheme.kind, int(bool(apply_scaling)),
-                                       ctypes.byref(self._ctx)))
+        _scheck(lib().wl_strips_create_ex(w, h, rank, nranks, levels, scheme.wavelet.index,
+                                          scheme.kind, _index(BOUNDARIES, boundary, "boundary"),
+                                          int(bool(apply_scaling)), ctypes.byref(self._ctx)))
         import torch
         self.input = torch.as_tensor(_DevView(lib().wl_strips_input(self._ctx),
                                               (self.rows, w)), device="cuda")
@@ -673,6 +678,18 @@ class StripPyramid:
         if out is None:
             out = torch.empty(self.slice_elems(), device="cuda", dtype=torch.float32)
         _scheck(lib().wl_strips_forward(self._ctx, out.data_ptr(), _stream_ptr(stream)))
+        return out
+
+    def inverse(self, slice_, out=None, stream=None):
+        """multi_level_inverse of this rank's slice -> its (rows, w) image rows."""
+        import torch
+        slice_ = _dev_f32(slice_, "slice").contiguous()
+        if slice_.numel() != self.slice_elems():
+            raise ValueError("slice size does not match this rank's pyramid slice")
+        if out is None:
+            out = torch.empty((self.rows, self.w), device="cuda", dtype=torch.float32)
+        _scheck(lib().wl_strips_inverse(self._ctx, slice_.data_ptr(), out.data_ptr(),
+                                        _stream_ptr(stream)))
         return out
 
     def check(self):
@@ -718,13 +735,13 @@ def stitch_strip_pyramid(slices, w, h, levels):
 
 
 def strip_pyramid_distributed(img_rows, w, h, levels, scheme: Scheme, group=None,
-                              apply_scaling=False):
+                              apply_scaling=False, boundary="periodic"):
     """Builds and connects this rank's StripPyramid over torch.distributed
     (blobs exchanged with all_gather_object; ring neighbours) and fills its
     input with `img_rows` (rows x w on this rank's GPU)."""
     import torch.distributed as dist
     rank, n = dist.get_rank(group), dist.get_world_size(group)
-    sp = StripPyramid(w, h, levels, scheme, rank, n, apply_scaling)
+    sp = StripPyramid(w, h, levels, scheme, rank, n, apply_scaling, boundary)
     if n > 1:
         blobs = [None] * n
         dist.all_gather_object(blobs, sp.export(), group=group)

@@ -291,7 +291,8 @@ int wl_dwt2_forward_strip(const float* strip, int w, int rows, int halo_rows, lo
                           int wavelet, int scheme, int scaling, float* ll, float* hl, float* lh,
                           float* hh, long plane_pitch, void* stream) {
     return wl_forward_strip_wait(strip, w, rows, halo_rows, pitch, wavelet, scheme, scaling, ll,
-                                 hl, lh, hh, plane_pitch, stream, nullptr, nullptr, 0, nullptr);
+                                 hl, lh, hh, plane_pitch, stream, nullptr, nullptr, 0, nullptr,
+                                 WL_PERIODIC, -1, -1);
 }
 
 }  // extern "C"
@@ -300,35 +301,48 @@ bool wl_strip_wait_capable(int wavelet, int scheme) {
     return !wl_host_program(prog_index(wavelet, scheme, 0)).is_conv;
 }
 
+static bool P_is_conv(int wavelet, int scheme) {
+    return wl_host_program(prog_index(wavelet, scheme, 0)).is_conv;
+}
+
 int wl_forward_strip_wait(const float* strip, int w, int rows, int halo_rows, long pitch,
                           int wavelet, int scheme, int scaling, float* ll, float* hl, float* lh,
                           float* hh, long plane_pitch, void* stream, const unsigned* xflag_a,
-                          const unsigned* xflag_b, unsigned xepoch, unsigned* xerr) {
+                          const unsigned* xflag_b, unsigned xepoch, unsigned* xerr,
+                          int boundary, int halo_top, int halo_bot) {
     if (w <= 0 || rows <= 0 || w % 2 != 0 || rows % 2 != 0)
         return fail(WL_EINVAL, "forward requires even positive dimensions");
     if (!valid_ids(wavelet, scheme, 0) || wavelet > WL_CDF97)
         return fail(WL_EINVAL, "strip transforms support cdf53/cdf97");
-    if (halo_rows % 2 != 0 || halo_rows < strip_halo(wavelet, 0))
-        return fail(WL_EINVAL, "strip halo too small (see wl_strip_halo_rows) or odd");
+    if (halo_top < 0) halo_top = halo_rows;
+    if (halo_bot < 0) halo_bot = halo_rows;
+    // periodic windows read a halo on both sides; a symmetric window may sit
+    // on the image's own top/bottom edge (halo 0 there: mirrored, exact)
+    const bool sym = boundary == WL_SYMMETRIC;
+    for (int hr : {halo_top, halo_bot})
+        if (hr % 2 != 0 || (hr < strip_halo(wavelet, 0) && !(sym && hr == 0)))
+            return fail(WL_EINVAL, "strip halo too small (see wl_strip_halo_rows) or odd");
     if (!strip || !ll || !hl || !lh || !hh) return fail(WL_EINVAL, "null buffer");
     if (pitch < w || plane_pitch < w / 2) return fail(WL_EINVAL, "pitch too small");
+    if (P_is_conv(wavelet, scheme) && sym)
+        return fail(WL_EINVAL, "symmetric strips need a lifting scheme");
     WlLevel L{};
-    L.in[0] = strip - static_cast<long>(halo_rows) * pitch;
+    L.in[0] = strip - static_cast<long>(halo_top) * pitch;
     L.out[0] = ll;
     L.out[1] = hl;
     L.out[2] = lh;
     L.out[3] = hh;
     L.qw = w / 2;
-    L.qh = rows / 2 + halo_rows;
+    L.qh = rows / 2 + (halo_top + halo_bot) / 2;
     L.in_pitch = pitch;
     L.out_pitch = plane_pitch;
     L.wavelet = wavelet;
     L.scheme = scheme;
     L.direction = 0;
     L.prog = prog_index(wavelet, scheme, 0);
-    L.boundary = WL_PERIODIC;
+    L.boundary = sym ? WL_SYMMETRIC : WL_PERIODIC;
     L.scaling = scaling != 0;
-    L.ylo = halo_rows / 2;
+    L.ylo = halo_top / 2;
     L.yhi = L.ylo + rows / 2;
     L.xflag_a = xflag_a;
     L.xflag_b = xflag_b;
@@ -350,10 +364,19 @@ bool wl_strip_shape_ok(int w, int rows, int halo_rows, int wavelet, int scheme, 
 }
 
 int wl_strip_mode(int w, int rows, int halo_rows, int wavelet, int scheme, int direction) {
+    return wl_strip_mode_b(w, rows, halo_rows, halo_rows, wavelet, scheme, direction, WL_PERIODIC);
+}
+
+int wl_strip_mode_b(int w, int rows, int halo_top, int halo_bot, int wavelet, int scheme,
+                    int direction, int boundary) {
+    const int halo_rows = halo_top;
     if (w <= 0 || rows <= 0 || !valid_ids(wavelet, scheme, 0) || wavelet > WL_CDF97) return 0;
     if (direction == 1 && scheme == WL_CONVOLUTION) scheme = WL_SWELDENS;
     const WlProgram& P = wl_host_program(prog_index(wavelet, scheme, direction));
-    if (P.is_conv) return w % 2 == 0 && rows % 2 == 0 ? 3 : 0;  // any even shape
+    if (P.is_conv) {
+        if (boundary == WL_SYMMETRIC) return 0;
+        return w % 2 == 0 && rows % 2 == 0 ? 3 : 0;  // any even shape
+    }
     // a level descriptor shaped like the strip call's, at dummy aligned addresses
     const float* dummy = reinterpret_cast<const float*>(static_cast<uintptr_t>(1) << 20);
     WlLevel L{};
@@ -361,28 +384,67 @@ int wl_strip_mode(int w, int rows, int halo_rows, int wavelet, int scheme, int d
     L.scheme = scheme;
     L.direction = direction;
     L.prog = prog_index(wavelet, scheme, direction);
-    L.boundary = WL_PERIODIC;
+    L.boundary = boundary;
     for (int k = 0; k < 4; ++k) {
         L.in[k] = dummy;
         L.out[k] = const_cast<float*>(dummy);
     }
     if (direction == 0) {
-        if (w % 2 || rows % 2 || halo_rows % 2) return false;
+        if (w % 2 || rows % 2 || halo_top % 2 || halo_bot % 2) return 0;
         L.qw = w / 2;
-        L.qh = rows / 2 + halo_rows;
+        L.qh = rows / 2 + (halo_top + halo_bot) / 2;
         L.in_pitch = w;
         L.out_pitch = w / 2;
-        L.ylo = halo_rows / 2;
+        L.ylo = halo_top / 2;
         L.yhi = L.ylo + rows / 2;
     } else {
         L.qw = w;
-        L.qh = rows + 2 * halo_rows;
+        L.qh = rows + halo_top + halo_bot;
         L.in_pitch = w;
         L.out_pitch = 2 * w;
-        L.ylo = halo_rows;
-        L.yhi = halo_rows + rows;
+        L.ylo = halo_top;
+        L.yhi = halo_top + rows;
     }
+    (void)halo_rows;
     return wl_fast_mode(L);
+}
+
+int wl_inverse_strip_ex(const float* ll, const float* hl, const float* lh, const float* hh,
+                        int qw, int qrows, int halo_top, int halo_bot, long plane_pitch,
+                        int wavelet, int scheme, int undo_scaling, float* img, long img_pitch,
+                        void* stream, int boundary) {
+    if (qw <= 0 || qrows <= 0) return fail(WL_EINVAL, "inverse requires positive plane dimensions");
+    if (!valid_ids(wavelet, scheme, 0) || wavelet > WL_CDF97)
+        return fail(WL_EINVAL, "strip transforms support cdf53/cdf97");
+    const bool sym = boundary == WL_SYMMETRIC;
+    for (int hr : {halo_top, halo_bot})
+        if (hr < strip_halo(wavelet, 1) && !(sym && hr == 0))
+            return fail(WL_EINVAL, "strip halo too small (see wl_strip_halo_rows)");
+    if (!img || !ll || !hl || !lh || !hh) return fail(WL_EINVAL, "null buffer");
+    if (img_pitch < 2 * qw || plane_pitch < qw) return fail(WL_EINVAL, "pitch too small");
+    if (scheme == WL_CONVOLUTION) scheme = WL_SWELDENS;
+    const long back = static_cast<long>(halo_top) * plane_pitch;
+    WlLevel L{};
+    L.in[0] = ll - back;
+    L.in[1] = hl - back;
+    L.in[2] = lh - back;
+    L.in[3] = hh - back;
+    L.out[0] = img;
+    L.qw = qw;
+    L.qh = qrows + halo_top + halo_bot;
+    L.in_pitch = plane_pitch;
+    L.out_pitch = img_pitch;
+    L.wavelet = wavelet;
+    L.scheme = scheme;
+    L.direction = 1;
+    L.prog = prog_index(wavelet, scheme, 1);
+    L.boundary = sym ? WL_SYMMETRIC : WL_PERIODIC;
+    L.scaling = undo_scaling != 0;
+    L.ylo = halo_top;
+    L.yhi = halo_top + qrows;
+    if (!wl_fast_supported(L))
+        return fail(WL_EINVAL, "no strip kernel for this shape");
+    return cuda_status(wl_launch_fast(L, static_cast<cudaStream_t>(stream)), "fast_kernel");
 }
 
 extern "C" {
@@ -391,36 +453,9 @@ int wl_dwt2_inverse_strip(const float* ll, const float* hl, const float* lh, con
                           int qw, int qrows, int halo_qrows, long plane_pitch, int wavelet,
                           int scheme, int undo_scaling, float* img, long img_pitch,
                           void* stream) {
-    if (qw <= 0 || qrows <= 0) return fail(WL_EINVAL, "inverse requires positive plane dimensions");
-    if (!valid_ids(wavelet, scheme, 0) || wavelet > WL_CDF97)
-        return fail(WL_EINVAL, "strip transforms support cdf53/cdf97");
-    if (halo_qrows < strip_halo(wavelet, 1))
-        return fail(WL_EINVAL, "strip halo too small (see wl_strip_halo_rows)");
-    if (!img || !ll || !hl || !lh || !hh) return fail(WL_EINVAL, "null buffer");
-    if (img_pitch < 2 * qw || plane_pitch < qw) return fail(WL_EINVAL, "pitch too small");
-    if (scheme == WL_CONVOLUTION) scheme = WL_SWELDENS;
-    const long back = static_cast<long>(halo_qrows) * plane_pitch;
-    WlLevel L{};
-    L.in[0] = ll - back;
-    L.in[1] = hl - back;
-    L.in[2] = lh - back;
-    L.in[3] = hh - back;
-    L.out[0] = img;
-    L.qw = qw;
-    L.qh = qrows + 2 * halo_qrows;
-    L.in_pitch = plane_pitch;
-    L.out_pitch = img_pitch;
-    L.wavelet = wavelet;
-    L.scheme = scheme;
-    L.direction = 1;
-    L.prog = prog_index(wavelet, scheme, 1);
-    L.boundary = WL_PERIODIC;
-    L.scaling = undo_scaling != 0;
-    L.ylo = halo_qrows;
-    L.yhi = halo_qrows + qrows;
-    if (!wl_fast_supported(L))
-        return fail(WL_EINVAL, "strip transform needs 16-byte aligned buffers and pitches");
-    return cuda_status(wl_launch_fast(L, static_cast<cudaStream_t>(stream)), "fast_kernel");
+    return wl_inverse_strip_ex(ll, hl, lh, hh, qw, qrows, halo_qrows, halo_qrows, plane_pitch,
+                               wavelet, scheme, undo_scaling, img, img_pitch, stream,
+                               WL_PERIODIC);
 }
 
 size_t wl_pyramid_elems(int w, int h, int levels) {

@@ -22,7 +22,10 @@ namespace {
 #define WL_CONV_Q 4
 #endif
 // Row segments via lane-swizzled 16-byte loads + shuffles (1) or overlapping
-// 8-byte loads (0: 4-way shared-memory bank conflicts)
+// 8-byte loads (0: 4-way shared-memory bank conflicts). Measured
+// (profiles/tuning_r02_conv.txt): cdf53 -10..-14% with shuffles, cdf97
+// +14..16% (its 9 rows x 8 shuffles cost more than the conflicts), so the
+// shuffle layout serves cdf53 only.
 #ifndef WL_CONV_SHFL
 #define WL_CONV_SHFL 1
 #endif
@@ -112,7 +115,7 @@ __global__ void __launch_bounds__(NT) conv_fast_kernel(const __grid_constant__ C
         for (int q = 0; q < Q; ++q)
 #pragma unroll
             for (int c = 0; c < 4; ++c) acc[q][c] = 0.f;
-#if WL_CONV_SHFL
+        if constexpr (WL_CONV_SHFL && C::kCol1 == 2) {
         // Row segment of the lane's Q quads: its own 2Q pixels with two
         // 16-byte loads in a lane-swizzled order (every 8-lane phase covers
         // all 32 banks: conflict-free), the -kCol0 / kCol1 halo pixels from
@@ -145,7 +148,7 @@ __global__ void __launch_bounds__(NT) conv_fast_kernel(const __grid_constant__ C
             }
             C::template row<Y, Q>(seg, acc);
         });
-#else
+        } else {
         // pixel column of seg[0] inside the staged tile
         const int sx = 2 * Q * qb + MARGIN + C::kCol0;
         wlfast::sfor<C::kRow1 - C::kRow0 + 1>([&](auto y_) {
@@ -160,7 +163,7 @@ __global__ void __launch_bounds__(NT) conv_fast_kernel(const __grid_constant__ C
             }
             C::template row<Y, Q>(seg, acc);
         });
-#endif
+        }
         const int gy = r0 + qr, gx = c0 + Q * qb;
         if (gy >= a.yhi) continue;
         if (a.scaling) {

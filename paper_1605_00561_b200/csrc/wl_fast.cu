@@ -181,20 +181,32 @@ cudaError_t wl_launch_fast(const WlLevel& L, cudaStream_t stream) {
     // to the interpreter, which mirrors every out-of-image read per step.
     const int Y0 = plan.args.Y0, X0 = plan.args.X0;
     const int Y1 = Y0 + plan.tiles_y * plan.args.TH, X1 = X0 + plan.args.tiles_x * plan.args.TW;
-    if (L.yhi > 0) return cudaErrorNotSupported;  // windows are periodic-only
     WlRects fr{};
     fr.n = 4;
     fr.y0[0] = 0;  fr.x0[0] = 0;  fr.ny[0] = Y0;          fr.nx[0] = L.qw;       // top
     fr.y0[1] = Y1; fr.x0[1] = 0;  fr.ny[1] = L.qh - Y1;   fr.nx[1] = L.qw;       // bottom
     fr.y0[2] = Y0; fr.x0[2] = 0;  fr.ny[2] = Y1 - Y0;     fr.nx[2] = X0;         // left
     fr.y0[3] = Y0; fr.x0[3] = X1; fr.ny[3] = Y1 - Y0;     fr.nx[3] = L.qw - X1;  // right
+    // symmetric window: only the stored rows [ylo, yhi) of the frame, into
+    // outputs addressed from the window's first row
+    const int wy0 = L.yhi > 0 ? L.ylo : 0, wy1 = L.yhi > 0 ? L.yhi : L.qh;
+    for (int k = 0; k < 4; ++k) {
+        const int a = fr.y0[k] > wy0 ? fr.y0[k] : wy0;
+        const int b = fr.y0[k] + fr.ny[k] < wy1 ? fr.y0[k] + fr.ny[k] : wy1;
+        fr.y0[k] = a;
+        fr.ny[k] = b > a ? b - a : 0;
+    }
     const int nb = L.nb > 1 ? L.nb : 1;
     for (int b = 0; b < nb; ++b) {  // the frame of every image of a batch
         WlLevel Li = L;
         Li.nb = 1;
+        Li.ylo = Li.yhi = 0;
         for (int k = 0; k < 4; ++k) {
             if (Li.in[k]) Li.in[k] += b * L.in_bstride[k];
             if (Li.out[k]) Li.out[k] += b * L.out_bstride[k];
+            // row 0 of the virtual whole plane (never written outside [wy0, wy1))
+            if (Li.out[k] && wy0) Li.out[k] -= static_cast<long>(wy0) * L.out_pitch *
+                                               (L.direction == 0 ? 1 : 2);
         }
         e = wl_launch_interp_rects(Li, fr, stream);
         if (e != cudaSuccess) return e;

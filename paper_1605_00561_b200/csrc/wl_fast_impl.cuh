@@ -1424,7 +1424,13 @@ inline Plan plan_tiles(const WlLevel& L, int H, int R, int NW, int CPT, bool no_
     // whole-image grid too: border tiles mirror their ghost cells per step
     // (kernel `mtile`); otherwise only interior tiles run here and the frame
     // goes to the interpreter.
-    bool full_sym = L.boundary == 1 && L.yhi == 0 && L.qw >= 2 && L.qh >= 2 &&
+    // A symmetric WINDOW (strip of a symmetric row-strip pyramid) is planned
+    // as the whole buffer [0, qh): the buffer edges are either the image's own
+    // (mirrored, exact) or at least H + 1 halo rows away from every stored row
+    // (their wrong mirroring never reaches a stored cell); the stores keep to
+    // [ylo, yhi).
+    const bool sym_window = L.boundary == 1 && L.yhi > 0;
+    bool full_sym = L.boundary == 1 && L.qw >= 2 && L.qh >= 2 &&
                     L.qw % CPT == 0 && WL_SYM_FAST && !no_mirror;
     // Row offset of the symmetric grid: every tile whose compute rows hold
     // image row 0 must not have it as a warp's last row (its mirror source,
@@ -1444,13 +1450,14 @@ inline Plan plan_tiles(const WlLevel& L, int H, int R, int NW, int CPT, bool no_
             if (rows_ok(y0)) ysym = y0;
         full_sym = ysym > 0;
     }
-    const bool whole = L.boundary == 0 || L.yhi > 0 || full_sym;
+    const bool whole = L.boundary == 0 || (L.yhi > 0 && !sym_window) || full_sym;
     const int X0 = wide ? (whole ? 0 : HX) : H, Y0 = full_sym ? ysym : H + 1;
     const int tx0 = wide ? 0 : -1;  // periodic plans
     int tx, ty;
     int y0 = Y0;
     p.args.mirror = full_sym ? 1 : 0;
-    if (L.yhi > 0) {
+    if (sym_window && (L.ylo < 0 || L.yhi > L.qh || L.yhi <= L.ylo)) return p;  // ok = false
+    if (L.yhi > 0 && !sym_window) {
         if (L.boundary != 0 || L.ylo < H + 1 || L.yhi > L.qh - H - 1 || L.yhi <= L.ylo)
             return p;  // ok = false
         tx = (L.qw - X0 > 0 ? (L.qw - X0 + TW - 1) / TW : 0) - tx0;
@@ -1485,6 +1492,10 @@ inline Plan plan_tiles(const WlLevel& L, int H, int R, int NW, int CPT, bool no_
     p.args.TH = TH;
     p.args.qw = L.qw;
     p.args.qh = L.qh;
+    if (sym_window) {
+        p.args.ylo = L.ylo;
+        p.args.yhi = L.yhi;
+    }
     p.ok = tx > 0 && ty > 0 && (long)nb * tx * ty < (1l << 31);
     return p;
 }

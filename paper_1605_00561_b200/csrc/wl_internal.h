@@ -80,7 +80,8 @@ bool wl_strip_wait_capable(int wavelet, int scheme);
 int wl_forward_strip_wait(const float* strip, int w, int rows, int halo_rows, long pitch,
                           int wavelet, int scheme, int scaling, float* ll, float* hl, float* lh,
                           float* hh, long plane_pitch, void* stream, const unsigned* xflag_a,
-                          const unsigned* xflag_b, unsigned xepoch, unsigned* xerr);
+                          const unsigned* xflag_b, unsigned xepoch, unsigned* xerr,
+                          int boundary, int halo_top, int halo_bot);
 
 // Can the strip transforms run this shape on dense buffers (pitch = width)
 // at 256-byte aligned addresses? forward: w pixels x rows (+ halo_rows above
@@ -90,3 +91,15 @@ bool wl_strip_shape_ok(int w, int rows, int halo_rows, int wavelet, int scheme, 
 // ... and how: 0 unsupported, 1 fast engine with TMA (halo wait foldable into
 // the transform), 2 fast engine direct-load path, 3 convolution kernel.
 int wl_strip_mode(int w, int rows, int halo_rows, int wavelet, int scheme, int direction);
+// ... for a window with halo_top / halo_bot rows under `boundary` (a
+// symmetric window may have 0 halo rows on the image's own edge).
+int wl_strip_mode_b(int w, int rows, int halo_top, int halo_bot, int wavelet, int scheme,
+                    int direction, int boundary);
+
+// Inverse strip with per-side halo rows and a boundary (a symmetric window
+// may have 0 halo rows on the image's own edge); wl_dwt2_inverse_strip is
+// the periodic case.
+int wl_inverse_strip_ex(const float* ll, const float* hl, const float* lh, const float* hh,
+                        int qw, int qrows, int halo_top, int halo_bot, long plane_pitch,
+                        int wavelet, int scheme, int undo_scaling, float* img, long img_pitch,
+                        void* stream, int boundary);

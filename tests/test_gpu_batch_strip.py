@@ -191,6 +191,67 @@ def test_strip_pyramid_virtual_ranks(wl, wavelet):
             assert torch.equal(got, want), (s, n)
 
 
+def _virtual_ranks_fwd_inv(wl, img, levels, sch, n, boundary):
+    """Forward then inverse strip pyramid over n virtual ranks: (stitched
+    flat pyramid, stitched reconstructed image)."""
+    import torch
+    h, w = img.shape
+    ranks = [wl.StripPyramid(w, h, levels, sch, r, n, boundary=boundary) for r in range(n)]
+    if n > 1:
+        blobs = [r.export() for r in ranks]
+        for r in range(n):
+            ranks[r].connect(blobs[(r - 1) % n], blobs[(r + 1) % n])
+    rows = h // n
+    for r in range(n):
+        ranks[r].input.copy_(img[r * rows:(r + 1) * rows])
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream() for _ in range(n)]
+    outs = [torch.full((ranks[r].slice_elems(),), float("nan"), device="cuda") for r in range(n)]
+    recs = [torch.full((rows, w), float("nan"), device="cuda") for _ in range(n)]
+    torch.cuda.synchronize()
+    for _ in range(2):  # twice: the second call reuses the epoch protocol
+        for r in range(n):
+            ranks[r].forward(outs[r], stream=streams[r])
+        for r in range(n):
+            ranks[r].inverse(outs[r], out=recs[r], stream=streams[r])
+    torch.cuda.synchronize()
+    for r in ranks:
+        r.check()
+        r.close()
+    return wl.stitch_strip_pyramid(outs, w, h, levels), torch.cat(recs)
+
+
+@pytest.mark.parametrize("wavelet", ["cdf53", "cdf97"])
+def test_strip_pyramid_symmetric_and_inverse(wl, wavelet):
+    """Row strips under both boundaries, forward and inverse, vs the
+    whole-image multi_level_forward / multi_level_inverse
+    (transform.cpp:198-256): bit-identical where the arithmetic is exact
+    (cdf53 dyadic) or the plans coincide (periodic); cdf97 symmetric within
+    tolerance (the strip and the whole image may pick different border
+    plans: mirrored register tiles vs interpreter frame)."""
+    import torch
+    h, w, levels = 768, 256, 4
+    img = rand((h, w), 23, dyadic=(wavelet == "cdf53"))
+    for s in ("monolithic_star", "sweldens", "iwahashi"):
+        sch = wl.build_scheme(s, wavelet)
+        for b in ("periodic", "symmetric"):
+            want = wl.multi_level_forward(img, sch, levels, b).flat
+            want_rec = wl.multi_level_inverse(wl.Pyramid(want, w, h, levels), wavelet, b,
+                                              scheme=s)
+            exact = wavelet == "cdf53" or b == "periodic"
+            for n in (1, 2, 3, 4):
+                got, rec = _virtual_ranks_fwd_inv(wl, img, levels, sch, n, b)
+                if exact:
+                    assert torch.equal(got, want), (s, b, n)
+                    assert torch.equal(rec, want_rec), (s, b, n)
+                else:
+                    rng = (want.max() - want.min()).item()
+                    assert (got - want).abs().max().item() <= TOL * rng, (s, b, n)
+                    assert (rec - want_rec).abs().max().item() <= 3e-5, (s, b, n)
+                if b == "periodic" or s != "polyphase":
+                    assert (rec - img).abs().max().item() <= 3e-5, (s, b, n)
+
+
 def test_strip_pyramid_errors(wl):
     sch = wl.build_scheme("monolithic_star", "cdf97")
     with pytest.raises(ValueError):
@@ -201,6 +262,9 @@ def test_strip_pyramid_errors(wl):
         wl.StripPyramid(256, 256, 2, wl.build_scheme("sweldens", "dd137"), 0, 1)
     with pytest.raises(ValueError):  # width not divisible by 2^levels
         wl.StripPyramid(1100, 1024, 3, sch, 0, 2)
+    with pytest.raises(ValueError):  # symmetric strips need a lifting scheme
+        wl.StripPyramid(256, 256, 2, wl.build_scheme("convolution", "cdf97"), 0, 2,
+                        boundary="symmetric")
 
 
 @pytest.mark.parametrize("wavelet", ["cdf53", "cdf97"])

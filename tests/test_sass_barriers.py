@@ -44,15 +44,28 @@ def test_sass_barriers_equal_count_barriers():
     counts = barrier_counts(wl.LIB_PATH)
     programs = {k[:3] for k in counts}
     assert len(programs) == 2 * 9 * 2, sorted(programs)
-    # plain + mirroring variant; forwards also the fused two-level variant
-    assert len(counts) == 2 * len(programs) + 2 * 9, len(counts)
+    # plain + mirroring + direct-load variant; forwards also the fused
+    # two-level variant
+    assert len(counts) == 3 * len(programs) + 2 * 9, len(counts)
+    kinds = {"direct": 0, "fused": 0}
     for (w, s, d, name), n in counts.items():
         want = wl.build_scheme(s, w).info(0 if d == "fwd" else 1)["barriers"]
-        if name.endswith("ELb1EEEv14CUtensorMap_stS2_S2_S2_NS_5KArgsE"):
+        xf, mirror, fused, direct = variant_flags(name)
+        if fused:
             # fused two-level variant: the tile body is instantiated once per
             # level (one runs per tile), after the one data-availability barrier
             want = 1 + 2 * (want - 1)
+            kinds["fused"] += 1
+        kinds["direct"] += direct
         assert n == want, (w, s, d, n, want)
+    assert kinds == {"direct": 36, "fused": 18}, kinds
+
+
+def variant_flags(name):
+    """(XF, MIRROR, FUSED, DIRECT) template flags of a mangled fast_kernel."""
+    m = re.search(r"Lb(\d)ELb(\d)ELb(\d)ELb(\d)EEEv14CUtensorMap", name)
+    assert m, name
+    return tuple(int(x) for x in m.groups())
 
 
 def build_broken(epoch=1):
@@ -70,6 +83,6 @@ def test_broken_barrier_variant_drops_one_barrier():
         want = wl.build_scheme(s, w).info(0 if d == "fwd" else 1)["barriers"]
         # epoch 1 exists only for schemes with >= 2 barriers
         want = want - 1 if want >= 2 else want
-        if name.endswith("ELb1EEEv14CUtensorMap_stS2_S2_S2_NS_5KArgsE"):
+        if variant_flags(name)[2]:
             want = 1 + 2 * (want - 1)  # fused variant: one body per level
         assert n == want, (w, s, d, n, want)
