@@ -246,6 +246,11 @@ int wl_set_graphs(int on);
 /* Number of kernel launches this library issued so far (process-global;
  * a graph replay counts its kernel nodes). */
 long wl_launch_count(void);
+/* Tuning diagnostics only (no reference counterpart): a device buffer of
+ * 4 x grid uint64 that a -DWL_DIAG_TIMES build of the fast engine fills per
+ * CTA (entry, first tile ready, exit in %globaltimer ns, tiles processed).
+ * NULL (default) disables; production builds ignore it. */
+void wl_diag_set(void* dev_buf);
 
 #ifdef __cplusplus
 }

@@ -108,6 +108,9 @@ int strip_halo(int wavelet, int direction) {
 
 void wl_count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
+static unsigned long long* g_diag = nullptr;
+unsigned long long* wl_diag_ptr() { return g_diag; }
+
 int wl_engine() { return g_engine.load(); }
 
 int wl_fail(int code, const char* msg) { return fail(code, msg); }
@@ -125,6 +128,11 @@ int wl_set_engine(int engine) { return g_engine.exchange(engine); }
 int wl_set_level_fusion(int on) { return g_fuse.exchange(on ? 1 : 0); }
 
 long wl_launch_count(void) { return g_launches.load(); }
+
+// Tuning diagnostics: a device buffer of 4 x grid u64 that WL_DIAG_TIMES
+// builds of the fast engine fill per CTA (entry, first tile ready, exit,
+// tiles processed; %globaltimer ns). Null disables. Not part of the drop-in.
+void wl_diag_set(void* dev_buf) { g_diag = static_cast<unsigned long long*>(dev_buf); }
 
 int wl_resolve_index(int i, int n, int boundary) {
     // transform.cpp:59-72

@@ -3,14 +3,16 @@
 // The reference evaluates the four 2-D analysis filters F_ss' at subsampled
 // positions (transform.cpp:129-152; 64 / 256 taps per quad, schemes.cpp:
 // 177-181). This kernel stages a (2*TQY + taps) x (2*TQX + 8) pixel tile in
-// shared memory (TMA for interior tiles; wrapped/mirrored loads on the IMAGE
-// grid for border tiles, which is exact for a single-pass filter), then each
-// thread slides over the input pixel rows of a 1 x Q quad strip, keeping the
-// row segment and the 4*Q accumulators in registers. The only block barrier
+// shared memory by TMA (border tiles: the out-of-image pixels of the
+// zero-filled box are then overwritten with their wrapped/mirrored sources on
+// the IMAGE grid, which is exact for a single-pass filter), then each
+// thread slides over the input pixel rows of an M x 4 quad block, keeping the
+// row segment and the 16*M accumulators in registers. The only block barrier
 // is the data-availability one (count_barriers = 1). The taps are
-// compile-time constants (gen/conv_gen.cuh), summed in row-major order
-// instead of the reference's std::map order (tolerance regime; exact for
-// cdf53 on dyadic inputs).
+// compile-time constants (gen/conv_gen.cuh), summed filter row by filter row
+// with mirror-image pixel pairs added first (row2s) instead of the
+// reference's std::map order (tolerance regime; exact for cdf53 on dyadic
+// inputs). Two horizontally adjacent quad pairs share one packed FFMA2.
 #include <cuda.h>
 
 #include "gen/conv_gen.cuh"
@@ -18,38 +20,54 @@
 
 namespace {
 
-#ifndef WL_CONV_Q
-#define WL_CONV_Q 4
+// Thread block: M quad rows x Q = 4 quads (two packed pairs: quads (0, 2)
+// and (1, 3) share every tap, FFMA2 with the coefficient broadcast). The
+// thread slides down the 2M + 7 (cdf97) input pixel rows of its block once;
+// each staged row is loaded ONCE and feeds every output row whose filter
+// window covers it (instead of once per output row), so shared-memory
+// traffic per output is ~(2M + 8) / (9M) of the one-row version.
+#ifndef WL_CONV_M
+#define WL_CONV_M 2
 #endif
-// Row segments via lane-swizzled 16-byte loads + shuffles (1) or overlapping
-// 8-byte loads (0: 4-way shared-memory bank conflicts). Measured
-// (profiles/tuning_r02_conv.txt): cdf53 -10..-14% with shuffles, cdf97
-// +14..16% (its 9 rows x 8 shuffles cost more than the conflicts), so the
-// shuffle layout serves cdf53 only.
-#ifndef WL_CONV_SHFL
-#define WL_CONV_SHFL 1
+// Mirror-symmetric filter rows folded (x[c-d] + x[c+d] added once, shared by
+// the components with that centre column): 25 instead of 32 FP32 ops per
+// quad and input row for cdf97 (row2s), else every tap (row2).
+#ifndef WL_CONV_FOLD
+#define WL_CONV_FOLD 1
 #endif
 #ifndef WL_CONV_TQY
 #define WL_CONV_TQY 32
 #endif
-constexpr int TQX = 64, TQY = WL_CONV_TQY, Q = WL_CONV_Q, NT = 256;
-constexpr int MARGIN = 4;                 // staged pixel columns left of the tile
-constexpr int SW = 2 * TQX + 2 * MARGIN;  // staged row length (136 px)
+constexpr int TQX = 64, TQY = WL_CONV_TQY, Q = 4, QP = Q / 2, M = WL_CONV_M;
+constexpr int NT = (TQX / Q) * (TQY / M);  // threads per CTA
+constexpr int MARGIN = 4;                  // staged pixel columns left of the tile
+constexpr int SW = 2 * TQX + 2 * MARGIN;   // staged row length (136 px)
+static_assert(TQY % M == 0 && NT % 32 == 0, "conv block geometry");
 
 template <class C>
 struct ConvGeo {
     static constexpr int kRows = 2 * TQY + (C::kRow1 - C::kRow0);
     static constexpr int kBytes = kRows * SW * 4;
-    static constexpr int kSeg = 2 * Q + (C::kCol1 - C::kCol0);
+    static constexpr int kSpan = C::kCol1 - C::kCol0;      // taps per row - 1
+    static constexpr int kPairs = 2 * (QP - 1) + kSpan + 1;  // packed row segment
+    static_assert(C::kCol0 >= -MARGIN && 2 * Q + kSpan + (C::kCol0 + MARGIN) <= 16,
+                  "row segment inside the four 16-byte loads");
 };
 
+// Image-grid index resolution for border tiles (periodic wrap / whole-point
+// mirror, transform.cpp:59-72); one conditional step when the overshoot is
+// smaller than the image, the general loop otherwise.
 __device__ __forceinline__ int resolve(int i, int n, int boundary) {
     if (i >= 0 && i < n) return i;
     if (n == 1) return 0;
     if (boundary == 0) {
+        if (i < 0 && i + n >= 0) return i + n;
+        if (i >= n && i - n < n) return i - n;
         int m = i % n;
         return m < 0 ? m + n : m;
     }
+    if (i < 0 && -i < n) return -i;
+    if (i >= n && 2 * (n - 1) - i >= 0) return 2 * (n - 1) - i;
     while (i < 0 || i >= n) {
         if (i < 0) i = -i;
         if (i >= n) i = 2 * (n - 1) - i;
@@ -85,9 +103,9 @@ __global__ void __launch_bounds__(NT) conv_fast_kernel(const __grid_constant__ C
     // this grid is not persistent, dependents must not take its SM slots.
     wlfast::pdl_wait();
     const int py0 = 2 * r0 + C::kRow0, px0 = 2 * c0 - MARGIN;
-    const bool interior = a.has_map && py0 >= 0 && px0 >= 0 && py0 + G::kRows <= h &&
-                          px0 + SW <= w;
-    if (interior) {
+    const bool interior = py0 >= 0 && px0 >= 0 && py0 + G::kRows <= h && px0 + SW <= w;
+    if (a.has_map) {
+        // every tile through TMA; outside the image the box is zero-filled
         if (threadIdx.x == 0) {
             wlfast::mbar_init(bar, 1);
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -96,81 +114,84 @@ __global__ void __launch_bounds__(NT) conv_fast_kernel(const __grid_constant__ C
         }
         __syncthreads();  // barrier init visible before anyone waits on it
         wlfast::mbar_wait(bar, 0);
+        if (!interior) {
+            // border tile: overwrite the out-of-image pixels with their
+            // wrapped / mirrored sources (image grid, exact for one pass);
+            // one warp per staged row, whole rows only when the row is outside
+            const int xl = px0 < 0 ? -px0 : 0;               // columns [0, xl) outside
+            const int xr = px0 + SW > w ? w - px0 : SW;       // columns [xr, SW) outside
+            for (int y = threadIdx.x / 32; y < G::kRows; y += NT / 32) {
+                const int yy = py0 + y;
+                const bool row_out = yy < 0 || yy >= h;
+                const float* src = img + (long)resolve(yy, h, a.boundary) * a.in_pitch;
+                for (int x = threadIdx.x & 31; x < SW; x += 32)
+                    if (row_out || x < xl || x >= xr)
+                        px[y * SW + x] = src[resolve(px0 + x, w, a.boundary)];
+            }
+            __syncthreads();
+        }
     } else {
-        for (int i = threadIdx.x; i < G::kRows * SW; i += NT) {
-            const int y = i / SW, x = i - (i / SW) * SW;
-            const int ry = resolve(py0 + y, h, a.boundary), rx = resolve(px0 + x, w, a.boundary);
-            px[i] = img[(long)ry * a.in_pitch + rx];
+        // no tensor map (unaligned pitch / pointer): element-wise staging
+        for (int y = threadIdx.x / 32; y < G::kRows; y += NT / 32) {
+            const float* src = img + (long)resolve(py0 + y, h, a.boundary) * a.in_pitch;
+            for (int x = threadIdx.x & 31; x < SW; x += 32)
+                px[y * SW + x] = src[resolve(px0 + x, w, a.boundary)];
         }
         __syncthreads();  // the single data-availability barrier
     }
 
-    constexpr int kBlocksX = TQX / Q;
+    const int qb = threadIdx.x % (TQX / Q), mb = threadIdx.x / (TQX / Q);
+    wl2 acc[M][QP][4];
 #pragma unroll
-    for (int k = 0; k < (TQY * kBlocksX) / NT; ++k) {
-        const int blk = threadIdx.x + k * NT;
-        const int qr = blk / kBlocksX, qb = blk - (blk / kBlocksX) * kBlocksX;
-        float acc[Q][4];
+    for (int i = 0; i < M; ++i)
 #pragma unroll
-        for (int q = 0; q < Q; ++q)
+        for (int p = 0; p < QP; ++p)
 #pragma unroll
-            for (int c = 0; c < 4; ++c) acc[q][c] = 0.f;
-        if constexpr (WL_CONV_SHFL && C::kCol1 == 2) {
-        // Row segment of the lane's Q quads: its own 2Q pixels with two
-        // 16-byte loads in a lane-swizzled order (every 8-lane phase covers
-        // all 32 banks: conflict-free), the -kCol0 / kCol1 halo pixels from
-        // the neighbour lanes by shuffle (a half-warp spans one 64-quad tile
-        // row); only the segment's edge lanes read their halo from memory.
-        static_assert(Q == 4 && TQX == 64, "shuffle layout: 16 lanes x 4 quads per row");
-        constexpr int HL = -C::kCol0, HR = C::kCol1;
-        const int lane = threadIdx.x & 31, sw = (lane >> 2) & 1;
-        wlfast::sfor<C::kRow1 - C::kRow0 + 1>([&](auto y_) {
-            constexpr int Y = decltype(y_)::value + C::kRow0;
-            const float* own = px + (2 * qr + Y - C::kRow0) * SW + MARGIN + 2 * Q * qb;
-            const float4 u0 = *reinterpret_cast<const float4*>(own + 4 * sw);
-            const float4 u1 = *reinterpret_cast<const float4*>(own + 4 * (sw ^ 1));
-            const float4 lo = sw ? u1 : u0, hi = sw ? u0 : u1;
-            const float o[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
-            float seg[G::kSeg];
+            for (int c = 0; c < 4; ++c) acc[i][p][c] = 0ull;  // (+0.f, +0.f)
+    // staged pixel column of buf[0]: the lane's 2Q own pixels start at 8*qb + MARGIN
+    const float* base = px + (2 * M * mb) * SW + 2 * Q * qb;
+    constexpr int kOff = C::kCol0 + MARGIN;  // seg[i] = buf[i + kOff]
+    wlfast::sfor<2 * (M - 1) + (C::kRow1 - C::kRow0) + 1>([&](auto j_) {
+        constexpr int J = decltype(j_)::value;
+        const float* row = base + J * SW;
+        float buf[16];
 #pragma unroll
-            for (int i = 0; i < HL; ++i) seg[i] = __shfl_up_sync(0xffffffffu, o[8 - HL + i], 1, 16);
-#pragma unroll
-            for (int i = 0; i < 8; ++i) seg[HL + i] = o[i];
-#pragma unroll
-            for (int i = 0; i < HR; ++i) seg[HL + 8 + i] = __shfl_down_sync(0xffffffffu, o[i], 1, 16);
-            if (qb == 0) {
-#pragma unroll
-                for (int i = 0; i < HL; ++i) seg[i] = own[i - HL];
-            }
-            if (qb == kBlocksX - 1) {
-#pragma unroll
-                for (int i = 0; i < HR; ++i) seg[HL + 8 + i] = own[8 + i];
-            }
-            C::template row<Y, Q>(seg, acc);
-        });
-        } else {
-        // pixel column of seg[0] inside the staged tile
-        const int sx = 2 * Q * qb + MARGIN + C::kCol0;
-        wlfast::sfor<C::kRow1 - C::kRow0 + 1>([&](auto y_) {
-            constexpr int Y = decltype(y_)::value + C::kRow0;
-            const float* row = px + (2 * qr + Y - C::kRow0) * SW + sx;
-            float seg[G::kSeg];
-#pragma unroll
-            for (int i = 0; i < G::kSeg; i += 2) {
-                const float2 v = *reinterpret_cast<const float2*>(row + i);
-                seg[i] = v.x;
-                seg[i + 1] = v.y;
-            }
-            C::template row<Y, Q>(seg, acc);
-        });
+        for (int k = 0; k < 4; ++k) {
+            const float4 u = reinterpret_cast<const float4*>(row)[k];
+            buf[4 * k] = u.x; buf[4 * k + 1] = u.y; buf[4 * k + 2] = u.z; buf[4 * k + 3] = u.w;
         }
-        const int gy = r0 + qr, gx = c0 + Q * qb;
-        if (gy >= a.yhi) continue;
+        wl2 pr[G::kPairs];
+#pragma unroll
+        for (int i = 0; i < G::kPairs; ++i) pr[i] = wl_pk_keep(buf[i + kOff], buf[i + kOff + Q]);
+        wlfast::sfor<M>([&](auto m_) {
+            constexpr int MM = decltype(m_)::value;
+            constexpr int Y = J + C::kRow0 - 2 * MM;  // filter row of this input row
+            if constexpr (Y >= C::kRow0 && Y <= C::kRow1) {
+                if constexpr (WL_CONV_FOLD)
+                    C::template row2s<Y, QP>(pr, acc[MM]);
+                else
+                    C::template row2<Y, QP>(pr, acc[MM]);
+            }
+        });
+    });
+    const int gx = c0 + Q * qb;
+#pragma unroll
+    for (int i = 0; i < M; ++i) {
+        const int gy = r0 + M * mb + i;
+        if (gy >= a.yhi) break;
+        float o[Q][4];
+#pragma unroll
+        for (int p = 0; p < QP; ++p)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                o[p][c] = wl_lo(acc[i][p][c]);
+                o[p + QP][c] = wl_hi(acc[i][p][c]);
+            }
         if (a.scaling) {
 #pragma unroll
             for (int q = 0; q < Q; ++q) {
-                acc[q][0] *= a.scale;
-                acc[q][3] /= a.scale;
+                o[q][0] *= a.scale;
+                o[q][3] /= a.scale;
             }
         }
         const long off = (long)(gy - a.ylo) * a.out_pitch + gx;
@@ -178,15 +199,11 @@ __global__ void __launch_bounds__(NT) conv_fast_kernel(const __grid_constant__ C
         for (int c = 0; c < 4; ++c) {
             float* p = a.out[c] + b * a.out_bstride[c] + off;
             if (a.vec4 && gx + Q <= a.qw) {
-                static_assert(Q % 4 == 0, "float4 stores of Q quads");
-#pragma unroll
-                for (int q = 0; q < Q; q += 4)
-                    *reinterpret_cast<float4*>(p + q) =
-                        make_float4(acc[q][c], acc[q + 1][c], acc[q + 2][c], acc[q + 3][c]);
+                *reinterpret_cast<float4*>(p) = make_float4(o[0][c], o[1][c], o[2][c], o[3][c]);
             } else {
 #pragma unroll
                 for (int q = 0; q < Q; ++q)
-                    if (gx + q < a.qw) p[q] = acc[q][c];
+                    if (gx + q < a.qw) p[q] = o[q][c];
             }
         }
     }

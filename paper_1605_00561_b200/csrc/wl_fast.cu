@@ -2,10 +2,58 @@
 // hand-off to the interpreter, dispatch to the per-(wavelet, direction)
 // instantiation units wl_fast_<wavelet>_<dir>.cu).
 #include <cstdint>
+#include <cstdlib>
+#include <mutex>
 
 #include "wl_fast_impl.cuh"
 
 namespace wlfast {
+
+// Dynamic tile-claim counters (FastArgs::sched): one zeroed device ring per
+// device; a slot is {claim counter, exit counter} and the last CTA of the
+// launch using it resets it to zero. Eager launches cycle through the first
+// kEager slots (a slot is reused only after kEager further launches, far
+// beyond the launch queue); launches captured into a CUDA graph get a slot of
+// their own from the rest, never reused (a replay may run concurrently with
+// eager launches); none left -> nullptr (static round robin). WL_DYN=0 turns
+// dynamic claims off.
+unsigned* sched_slot(cudaStream_t stream) {
+    constexpr int kEager = 4096, kSlots = 8192;
+    static std::mutex mu;
+    static unsigned* ring[64] = {};
+    static int next_eager[64] = {}, next_cap[64] = {};
+    static const bool off = [] {
+        const char* e = getenv("WL_DYN");
+        return e && e[0] == '0';
+    }();
+    if (off) return nullptr;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev >= 64) return nullptr;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(stream, &cs) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    std::lock_guard<std::mutex> lk(mu);
+    if (!ring[dev]) {
+        if (cs != cudaStreamCaptureStatusNone) return nullptr;  // no allocation while capturing
+        unsigned* p = nullptr;
+        if (cudaMalloc(&p, sizeof(unsigned) * 2 * kSlots) != cudaSuccess ||
+            cudaMemset(p, 0, sizeof(unsigned) * 2 * kSlots) != cudaSuccess ||
+            cudaDeviceSynchronize() != cudaSuccess) {
+            cudaGetLastError();
+            return nullptr;
+        }
+        ring[dev] = p;
+    }
+    if (cs != cudaStreamCaptureStatusNone) {
+        if (kEager + next_cap[dev] >= kSlots) return nullptr;
+        return ring[dev] + 2 * (kEager + next_cap[dev]++);
+    }
+    const int k = next_eager[dev];
+    next_eager[dev] = (k + 1) % kEager;
+    return ring[dev] + 2 * k;
+}
 
 EncodeTiledFn encode_fn() {
     static EncodeTiledFn fn = [] {
@@ -232,8 +280,8 @@ cudaError_t wl_launch_fast_fused(const WlLevel& L0, const WlLevel& L1, unsigned*
     int R, NW, CPT;
     geometry(L0, &R, &NW, &CPT);
     const int H = wl_host_program(L0.prog).halo;
-    const wlfast::Plan p0 = wlfast::plan_tiles(L0, H, R, NW, CPT);
-    const wlfast::Plan p1 = wlfast::plan_tiles(L1, H, R, NW, CPT);
+    const wlfast::Plan p0 = wlfast::plan_tiles(L0, H, R, NW, CPT, false, true);
+    const wlfast::Plan p1 = wlfast::plan_tiles(L1, H, R, NW, CPT, false, true);
     if (!p0.ok || !p1.ok) return cudaErrorNotSupported;
     const int nb = L0.nb > 1 ? L0.nb : 1;
     if (2 + static_cast<size_t>(nb) * p0.tiles_y > wl_fused_ctr_elems(L0.qh, nb))

@@ -208,6 +208,8 @@ struct FastArgs {
     int ntiles_img;      // tiles per image
     int tx0, ty0;        // index of the first tile column / row (-1 when covering borders)
     int X0, Y0;          // first output cell of tile (0, 0)
+    int xlast, ylast;    // tile origins clamped to these (last tile column / row
+                         // ends at the image edge, overlapping its neighbour)
     int TW, TH;          // output tile size in cells
     int wrap;            // periodic plan covering the whole image (border tiles wrap)
     int scaling;
@@ -221,6 +223,12 @@ struct FastArgs {
     const unsigned* xflag_b;
     unsigned xepoch;
     unsigned* xerr;
+    // dynamic tile claims: {claim counter, exit counter}, zero at launch and
+    // reset by the last CTA to exit (wl_sched_slot); null = static round robin
+    unsigned* sched;
+    // WL_DIAG_TIMES builds only: per CTA {entry, first tile ready, exit, tiles}
+    // (%globaltimer ns), wl_diag_set(); null otherwise
+    unsigned long long* diag;
 };
 
 // Tile-row order: with a halo wait the window's first and last tile rows go
@@ -282,6 +290,16 @@ struct KArgs {
 
 __device__ __host__ __forceinline__ int floordiv(int a, int b) {
     return a >= 0 ? a / b : -((-a + b - 1) / b);
+}
+// First stored cell column / row of tile column tx / row ty (grid indices
+// already offset by tx0 / ty0).
+__device__ __forceinline__ int tile_xs(const FastArgs& a, int tx) {
+    const int x = a.X0 + tx * a.TW;
+    return x < a.xlast ? x : a.xlast;
+}
+__device__ __forceinline__ int tile_ys(const FastArgs& a, int ty) {
+    const int y = a.Y0 + ty * a.TH;
+    return y < a.ylast ? y : a.ylast;
 }
 __device__ __forceinline__ unsigned ld_relaxed_gpu_u32(const unsigned* p) {
     unsigned v;
@@ -416,6 +434,39 @@ struct Acc {
     }
 };
 
+// Packed pair of cells (CC, CC + S) of row RR for the FFMA2 neighbour code
+// (P::nbr2): both cells run the scalar code's operation sequence, one packed
+// instruction per tap for the two of them.
+template <int R, int CPT, int RR, int CC, int S>
+struct Acc2 {
+    Acc<R, CPT, RR, CC> a0;
+    Acc<R, CPT, RR, CC + S> a1;
+    template <int C, int DR, int DC>
+    __device__ __forceinline__ wl2 g() const {
+        return wl_pk(a0.template g<C, DR, DC>(), a1.template g<C, DR, DC>());
+    }
+};
+// Pair stride per program (0 = scalar FFMA code). FP32-issue-bound programs
+// (cdf97 Polyphase: 126 MACs per cell) issue half the FMA instructions packed.
+#ifndef WL_PAIR_POLY
+#define WL_PAIR_POLY 0
+#endif
+#ifndef WL_PAIR_ALL
+#define WL_PAIR_ALL 0
+#endif
+template <class P>
+struct PairStride {
+    static constexpr int S = WL_PAIR_ALL;
+};
+template <>
+struct PairStride<P_cdf97_polyphase_fwd> {
+    static constexpr int S = WL_PAIR_POLY;
+};
+template <>
+struct PairStride<P_cdf97_polyphase_inv> {
+    static constexpr int S = WL_PAIR_POLY;
+};
+
 // kUse bit layout (gen_steps.py usage_mask): comp*9 + (dr+1)*3 + (dc+1).
 __host__ __device__ constexpr bool uses(unsigned long long m, int c, int dr, int dc) {
     return (m >> (c * 9 + (dr + 1) * 3 + (dc + 1))) & 1ull;
@@ -499,6 +550,16 @@ __global__ void __launch_bounds__((NW + 1) * 32,
 
     const FastArgs& a = K.lv[0];  // per-tile code rebinds it to the tile's level
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#ifdef WL_DIAG_TIMES
+    auto gtime = [] {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        return t;
+    };
+    unsigned long long* dg = a.diag ? a.diag + 4 * blockIdx.x : nullptr;
+    if (dg && threadIdx.x == 0) dg[0] = gtime();
+    int diag_tiles = 0;
+#endif
     if (threadIdx.x == 0) {
         for (int k = 0; k < NS; ++k) {
             mbar_init(&full[k], 1);
@@ -664,8 +725,8 @@ __global__ void __launch_bounds__((NW + 1) * 32,
                     break;
                 }
                 const FastArgs& a = K.lv[lvl];
-                const int cx = a.X0 + (txi + a.tx0) * a.TW - HX;
-                const int cy = a.Y0 + (tyi + a.ty0) * a.TH - H - 1;
+                const int cx = tile_xs(a, txi + a.tx0) - HX;
+                const int cy = tile_ys(a, tyi + a.ty0) - H - 1;
                 if (i >= NS) wait_empty(s, (use - 1) & 1);
                 report(i - kRing + 1, true);  // ring slot i % kRing is free
                 row_ring[i & (kRing - 1)] = lvl == 0 ? b * f.R0 + tyi : -1;
@@ -680,14 +741,76 @@ __global__ void __launch_bounds__((NW + 1) * 32,
                                 2 * cy + q * kSplitRows, b);
                 if (p1 < f.n1) prefetch();
             }
+        } else if (lane == 0 && a.sched) {
+            // Dynamic tile claims: the first tile is blockIdx.x, every further
+            // one comes from a global counter, so CTAs on SMs that run ahead
+            // take more tiles and the launch's tail shrinks (static round robin
+            // left 7-20 us between the first and the last CTA to finish at
+            // 8192^2, tools/diag_times.py). The tile index goes to the compute
+            // warps through task_sm; -1 ends their loop.
+            bool halo_ready = false;
+            int t = blockIdx.x;
+            for (int i = 0;; ++i) {
+                const int s = i % NS;
+                const unsigned use = i / NS;
+                if (a.filter) {  // interior-only / border-only launch of a symmetric plan
+                    for (; t < a.ntiles; t = gridDim.x + (int)atomicAdd(a.sched, 1u)) {
+                        const int fb = t / a.ntiles_img, ft = t - fb * a.ntiles_img;
+                        const int fy = ft / a.tiles_x;
+                        const int fx0 = tile_xs(a, ft - fy * a.tiles_x + a.tx0) - HX;
+                        const int fy0 = tile_ys(a, fy + a.ty0) - H - 1;
+                        const bool bd = fx0 < 0 || fy0 < 0 || fx0 + TWC > a.qw || fy0 + G::kRows > a.qh;
+                        if (bd == (a.filter == 2)) break;
+                    }
+                }
+                if (i >= NS) mbar_wait_backoff<ProdBackoff<P, DIR>::ns>(&empty[s], (use - 1) & 1);
+                if (t >= a.ntiles) {
+                    task_sm[s] = make_int4(-1, 0, 0, 0);
+                    mbar_arrive(&full[s]);  // consumers see the sentinel and stop
+                    break;
+                }
+                task_sm[s] = make_int4(t, 0, 0, 0);
+                const int b = t / a.ntiles_img, tt = t - b * a.ntiles_img;
+                const int tyk = tt / a.tiles_x;
+                const int tyi = a.xflag_a ? tile_row_of(tyk, a.ntiles_img / a.tiles_x, true) : tyk;
+                const int ty = tyi + a.ty0, tx = tt - tyk * a.tiles_x + a.tx0;
+                const int cx = tile_xs(a, tx) - HX;
+                const int cy = tile_ys(a, ty) - H - 1;
+                if (a.xflag_a && !halo_ready && (cy < a.ylo || cy + G::kRows > a.yhi)) {
+                    wait_halo_flags(a.xflag_a, a.xflag_b, a.xepoch, a.xerr);
+                    halo_ready = true;
+                }
+                float* dst = stage + s * G::kStageFloats;
+                mbar_expect_tx(&full[s], G::kStageBytes);
+                if (DIR == 0) {
+                    constexpr int kSplitRows = 2 * G::kRows / WL_FWD_SPLIT;
+#pragma unroll
+                    for (int q = 0; q < WL_FWD_SPLIT; ++q)
+                        tma_load_3d(dst + q * kSplitRows * 2 * TWC, &m0, &full[s], 2 * cx,
+                                    2 * cy + q * kSplitRows, b);
+                } else {
+                    constexpr int plane = TWC * G::kRows;
+                    tma_load_3d(dst, &m0, &full[s], cx, cy, b);
+                    tma_load_3d(dst + plane, &m1, &full[s], cx, cy, b);
+                    tma_load_3d(dst + 2 * plane, &m2, &full[s], cx, cy, b);
+                    tma_load_3d(dst + 3 * plane, &m3, &full[s], cx, cy, b);
+                }
+                t = gridDim.x + (int)atomicAdd(a.sched, 1u);  // next claim overlaps the load
+            }
+            // the last producer out resets the slot for the next launch using it
+            // (every producer's final claim precedes its exit count)
+            if (atomicAdd(a.sched + 1, 1u) == gridDim.x - 1) {
+                a.sched[0] = 0;
+                a.sched[1] = 0;
+            }
         } else if (lane == 0) {
             bool halo_ready = false;
             for (int i = 0, t = blockIdx.x; t < a.ntiles; t += gridDim.x) {
                 if (a.filter) {  // interior-only / border-only launch of a symmetric plan
                     const int fb = t / a.ntiles_img, ft = t - fb * a.ntiles_img;
                     const int fy = ft / a.tiles_x;
-                    const int fx0 = a.X0 + (ft - fy * a.tiles_x + a.tx0) * a.TW - HX;
-                    const int fy0 = a.Y0 + (fy + a.ty0) * a.TH - H - 1;
+                    const int fx0 = tile_xs(a, ft - fy * a.tiles_x + a.tx0) - HX;
+                    const int fy0 = tile_ys(a, fy + a.ty0) - H - 1;
                     const bool bd = fx0 < 0 || fy0 < 0 || fx0 + TWC > a.qw || fy0 + G::kRows > a.qh;
                     if (bd != (a.filter == 2)) continue;
                 }
@@ -700,8 +823,8 @@ __global__ void __launch_bounds__((NW + 1) * 32,
                 const int tyk = tt / a.tiles_x;
                 const int tyi = a.xflag_a ? tile_row_of(tyk, a.ntiles_img / a.tiles_x, true) : tyk;
                 const int ty = tyi + a.ty0, tx = tt - tyk * a.tiles_x + a.tx0;
-                const int cx = a.X0 + tx * a.TW - HX;     // first compute cell column
-                const int cy = a.Y0 + ty * a.TH - H - 1;  // ghost row above the region
+                const int cx = tile_xs(a, tx) - HX;     // first compute cell column
+                const int cy = tile_ys(a, ty) - H - 1;  // ghost row above the region
                 if (a.xflag_a && !halo_ready && (cy < a.ylo || cy + G::kRows > a.yhi)) {
                     wait_halo_flags(a.xflag_a, a.xflag_b, a.xepoch, a.xerr);
                     halo_ready = true;
@@ -751,6 +874,11 @@ __global__ void __launch_bounds__((NW + 1) * 32,
             txi = tk.w;
         } else {
             const FastArgs& a0 = K.lv[0];
+            if (!DIRECT && a0.sched) {  // dynamic claims: the producer names the tile
+                mbar_wait(&full[s], (i / NS) & 1);
+                t = task_sm[s].x;
+                if (t < 0) break;
+            }
             if (t >= a0.ntiles) break;
             b = t / a0.ntiles_img;
             const int tt = t - b * a0.ntiles_img;
@@ -763,8 +891,8 @@ __global__ void __launch_bounds__((NW + 1) * 32,
         auto body = [&](auto L_) {
             const FastArgs& a = K.lv[decltype(L_)::value];
             const int ty = tyi + a.ty0, tx = txi + a.tx0;
-            const int cx = a.X0 + tx * a.TW - HX;     // first compute cell column
-            const int cy = a.Y0 + ty * a.TH - H - 1;  // ghost row above the region
+            const int cx = tile_xs(a, tx) - HX;     // first compute cell column
+            const int cy = tile_ys(a, ty) - H - 1;  // ghost row above the region
             // Border tile: its compute region leaves the image. Periodic plans
             // load its cells with wrapped coordinates straight from global memory
             // (load-time wrap is exact for the periodic extension).
@@ -780,44 +908,53 @@ __global__ void __launch_bounds__((NW + 1) * 32,
             // the distance-1 ghosts are overwritten with their mirror images.
             const bool mtile = MIRROR && a.mirror && border;
             const int gy0m = cy + 1 + warp * R;  // image row of v[0]
-            if constexpr (!FUSED && !DIRECT) mbar_wait(&full[s], phase);
+            if constexpr (!FUSED && !DIRECT)
+                if (!a.sched) mbar_wait(&full[s], phase);  // (dynamic: waited for the task)
+#ifdef WL_DIAG_TIMES
+            if (dg && threadIdx.x == 0 && diag_tiles++ == 0) dg[1] = gtime();
+#endif
             const float* st = stage + s * G::kStageFloats;
 
             // Load the warp's rows (+ one ghost row above and below) and split
             // the 2x2 polyphase components.
+            // periodic wrap: one conditional add/subtract unless the image is
+            // smaller than a tile (then the general modulo)
+            const bool small = WL_WRAP_MOD_INV && DIR == 1 || a.qw < TWC || a.qh < G::kRows;
+            auto wrapi = [small](int i, int n) {
+                if (small) {
+                    i %= n;
+                    return i < 0 ? i + n : i;
+                }
+                return i < 0 ? i + n : (i >= n ? i - n : i);
+            };
+            // one cell (image cell row ry, column rx, already wrapped) from global memory
+            auto load_cell = [&](int ry, int rx, float (&c4)[4]) {
+                if (DIR == 0) {
+                    const float* p =
+                        a.in[0] + b * a.in_bstride[0] + (long)(2 * ry) * a.in_pitch + 2 * rx;
+                    const float2 u0 = *reinterpret_cast<const float2*>(p);
+                    const float2 u1 = *reinterpret_cast<const float2*>(p + a.in_pitch);
+                    c4[0] = u0.x;
+                    c4[1] = u0.y;
+                    c4[2] = u1.x;
+                    c4[3] = u1.y;
+                } else {
+#pragma unroll
+                    for (int c = 0; c < 4; ++c)
+                        c4[c] = a.in[c][b * a.in_bstride[c] + (long)ry * a.in_pitch + rx];
+                }
+            };
+            // Load the warp's rows (+ one ghost row above and below) and split
+            // the 2x2 polyphase components.
             auto load_row = [&](int q, float (&dst)[CPT][4]) {
                 // q: cell row in the stage (0 = ghost row above the region)
-                if (wrap_tile) {
-                    // periodic wrap: one conditional add/subtract unless the image
-                    // is smaller than a tile (then the general modulo)
-                    const bool small = WL_WRAP_MOD_INV && DIR == 1 || a.qw < TWC || a.qh < G::kRows;
-                    auto wrapi = [small](int i, int n) {
-                        if (small) {
-                            i %= n;
-                            return i < 0 ? i + n : i;
-                        }
-                        return i < 0 ? i + n : (i >= n ? i - n : i);
-                    };
+                if (DIRECT) {
                     const int ry = wrapi(cy + q, a.qh);
 #pragma unroll
-                    for (int j = 0; j < CPT; ++j) {
-                        const int rx = wrapi(cx + CPT * lane + j, a.qw);
-                        if (DIR == 0) {
-                            const float* p =
-                                a.in[0] + b * a.in_bstride[0] + (long)(2 * ry) * a.in_pitch + 2 * rx;
-                            const float2 u0 = *reinterpret_cast<const float2*>(p);
-                            const float2 u1 = *reinterpret_cast<const float2*>(p + a.in_pitch);
-                            dst[j][0] = u0.x;
-                            dst[j][1] = u0.y;
-                            dst[j][2] = u1.x;
-                            dst[j][3] = u1.y;
-                        } else {
-#pragma unroll
-                            for (int c = 0; c < 4; ++c)
-                                dst[j][c] = a.in[c][b * a.in_bstride[c] + (long)ry * a.in_pitch + rx];
-                        }
-                    }
-                } else if (DIR == 0) {
+                    for (int j = 0; j < CPT; ++j) load_cell(ry, wrapi(cx + CPT * lane + j, a.qw), dst[j]);
+                    return;
+                }
+                if (DIR == 0) {
                     // pixel rows 2q (LL HL LL HL ...) and 2q+1 (LH HH ...)
                     const float* p0 = st + (2 * q) * (2 * TWC) + 2 * CPT * lane;
                     float4 e[CPT / 2], o[CPT / 2];
@@ -865,6 +1002,20 @@ __global__ void __launch_bounds__((NW + 1) * 32,
                             dst[0][c] = u.x;
                             dst[1][c] = u.y;
                         }
+                    }
+                }
+                if (wrap_tile) {
+                    // Border tile of a periodic plan: the TMA box is zero-filled
+                    // outside the image; only those cells are re-read from their
+                    // wrapped positions (exact for the periodic extension). The
+                    // row test is warp-uniform; columns diverge on edge lanes only.
+                    const int yq = cy + q;
+                    const bool row_in = yq >= 0 && yq < a.qh;
+                    const int ry = row_in ? yq : wrapi(yq, a.qh);
+#pragma unroll
+                    for (int j = 0; j < CPT; ++j) {
+                        const int xq = cx + CPT * lane + j;
+                        if (!row_in || xq < 0 || xq >= a.qw) load_cell(ry, wrapi(xq, a.qw), dst[j]);
                     }
                 }
             };
@@ -1027,12 +1178,29 @@ __global__ void __launch_bounds__((NW + 1) * 32,
                 });
                 if constexpr (MIRROR) hfix(sl, sr, 1, R);
                 float o[R][CPT][4];
+                constexpr int PS = PairStride<P>::S < CPT ? PairStride<P>::S : 0;
                 auto row = [&](auto r_) {
-                    sfor<CPT>([&](auto c_) {
-                        constexpr int RR = decltype(r_)::value, CC = decltype(c_)::value;
-                        Acc<R, CPT, RR, CC> acc{v, gu, gd, sl, sr};
-                        P::template nbr<E>(acc, o[RR][CC]);
-                    });
+                    constexpr int RR = decltype(r_)::value;
+                    if constexpr (PS > 0) {
+                        sfor<CPT / 2>([&](auto p_) {
+                            constexpr int p = decltype(p_)::value;
+                            constexpr int C0 = (p / PS) * 2 * PS + p % PS, C1 = C0 + PS;
+                            Acc2<R, CPT, RR, C0, PS> acc{{v, gu, gd, sl, sr}, {v, gu, gd, sl, sr}};
+                            wl2 o2[4];
+                            P::template nbr2<E>(acc, o2);
+#pragma unroll
+                            for (int k = 0; k < 4; ++k) {
+                                o[RR][C0][k] = wl_lo(o2[k]);
+                                o[RR][C1][k] = wl_hi(o2[k]);
+                            }
+                        });
+                    } else {
+                        sfor<CPT>([&](auto c_) {
+                            constexpr int CC = decltype(c_)::value;
+                            Acc<R, CPT, RR, CC> acc{v, gu, gd, sl, sr};
+                            P::template nbr<E>(acc, o[RR][CC]);
+                        });
+                    }
                 };
                 // interior rows 1..R-2 read only this warp's rows
                 sfor<R - 2>([&](auto r_) { row(std::integral_constant<int, decltype(r_)::value + 1>{}); });
@@ -1214,6 +1382,12 @@ __global__ void __launch_bounds__((NW + 1) * 32,
             body(std::integral_constant<int, 0>{});
         }
     }
+#ifdef WL_DIAG_TIMES
+    if (dg && threadIdx.x == 0) {
+        dg[2] = gtime();
+        dg[3] = diag_tiles;
+    }
+#endif
 }
 
 // ------------------------------------------------------------------ host side
@@ -1222,6 +1396,8 @@ using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t
                                    const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
                                    CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 EncodeTiledFn encode_fn();
+// Claim-counter slot for a launch on `stream` (wl_fast.cu); nullptr = static.
+unsigned* sched_slot(cudaStream_t stream);
 
 // 3-D map (w, h, nb images at `bstride` elements apart) of a float32 buffer;
 // box = box_w x box_h x 1.
@@ -1403,8 +1579,18 @@ struct Plan {
 //    [ylo, yhi) only; the rows around them are halo rows physically present
 //    in the buffer (ylo >= H + 1 and yhi <= qh - H - 1 keep every stored
 //    cell's dependency cone and the tiles' ghost rows inside the buffer).
-inline Plan plan_tiles(const WlLevel& L, int H, int R, int NW, int CPT, bool no_mirror = false) {
+//  * periodic plans (whole image or strip window) other than the fused
+//    launches' (`legacy`): tile (0, 0) stores cell (0, 0) onwards -- only its
+//    reach + 1 ghost rows / halo columns wrap -- and the last tile row /
+//    column is clamped to end at the image edge (overlapping its neighbour,
+//    which writes the same values), so no tile computes wrapped cells it does
+//    not store: the former plan (first row/column of tiles BEFORE the image,
+//    last ones past its end) cost 7-10% redundant work at 8192^2 and its
+//    nearly-all-wrapped edge tiles made the launch's tail.
+inline Plan plan_tiles(const WlLevel& L, int H, int R, int NW, int CPT, bool no_mirror = false,
+                       bool legacy = false) {
     Plan p{};
+    p.args.xlast = p.args.ylast = 0x7fffffff;
     const int nb = L.nb > 1 ? L.nb : 1;
     p.args.ylo = 0;
     p.args.yhi = L.qh;
@@ -1451,7 +1637,8 @@ inline Plan plan_tiles(const WlLevel& L, int H, int R, int NW, int CPT, bool no_
         full_sym = ysym > 0;
     }
     const bool whole = L.boundary == 0 || (L.yhi > 0 && !sym_window) || full_sym;
-    const int X0 = wide ? (whole ? 0 : HX) : H, Y0 = full_sym ? ysym : H + 1;
+    int X0 = wide ? (whole ? 0 : HX) : H;
+    const int Y0 = full_sym ? ysym : H + 1;
     const int tx0 = wide ? 0 : -1;  // periodic plans
     int tx, ty;
     int y0 = Y0;
@@ -1481,6 +1668,23 @@ inline Plan plan_tiles(const WlLevel& L, int H, int R, int NW, int CPT, bool no_
         ty = span >= NW * R + 2 ? (span - (NW * R + 2)) / TH + 1 : 0;
         p.args.tx0 = p.args.ty0 = 0;
         p.args.wrap = 0;
+    }
+    if (L.boundary == 0 && !legacy && (whole || (L.yhi > 0 && !sym_window))) {
+        // X0 - HX = -4: box starts stay 16-byte aligned (TW = 0 mod 4 when CPT = 2)
+        const int Xp = wide ? 0 : H - 4;
+        tx = L.qw - Xp > 0 ? (L.qw - Xp + TW - 1) / TW : 0;
+        const int xr = L.qw - TW - Xp;  // last origin rounded UP to the 4-cell grid
+        p.args.xlast = Xp + (xr > 0 ? (xr + 3) / 4 * 4 : 0);
+        p.args.tx0 = 0;
+        X0 = Xp;
+        if (whole) {
+            ty = (L.qh + TH - 1) / TH;
+            y0 = 0;
+            p.args.ylast = L.qh - TH > 0 ? L.qh - TH : 0;
+            p.args.ty0 = 0;
+        } else {
+            p.args.ylast = L.yhi - TH > L.ylo ? L.yhi - TH : L.ylo;
+        }
     }
     p.args.tiles_x = tx;
     p.tiles_y = ty;
@@ -1532,6 +1736,7 @@ bool level_args(const WlLevel& L, const Plan& plan, FastArgs& a, CUtensorMap (&m
     a.xflag_b = L.xflag_b;
     a.xepoch = L.xepoch;
     a.xerr = L.xerr;
+    a.diag = wl_diag_ptr();
     a.in_pitch = L.in_pitch;
     a.out_pitch = L.out_pitch;
     a.scaling = L.scaling && wl_host_program(L.prog).has_scale;
@@ -1573,6 +1778,7 @@ cudaError_t launch(const WlLevel& L, const Plan& plan, cudaStream_t stream) {
         const int mb = grid_cap<R, NW, CPT, NS, NXC, MAXB>(kern, cache);
         KArgs f = k;
         f.lv[0].filter = filter;
+        f.lv[0].sched = f.lv[0].ntiles > mb ? sched_slot(stream) : nullptr;
         const int grid = f.lv[0].ntiles < mb ? f.lv[0].ntiles : mb;
         cudaError_t le = launch_pdl(kern, dim3(grid), dim3((NW + 1) * 32), G::kSmemBytes,
                                     stream, maps[0], maps[1], maps[2], maps[3], f);
@@ -1606,6 +1812,8 @@ cudaError_t launch_direct(const WlLevel& L, const Plan& plan, cudaStream_t strea
         a.out_bstride[q] = nb > 1 ? L.out_bstride[q] : 0;
     }
     a.xflag_a = a.xflag_b = nullptr;
+    a.sched = nullptr;  // no producer warp: static tiles
+    a.diag = wl_diag_ptr();
     a.in_pitch = L.in_pitch;
     a.out_pitch = L.out_pitch;
     a.scaling = L.scaling && wl_host_program(L.prog).has_scale;

@@ -71,6 +71,8 @@ cudaError_t wl_launch_fast_fused(const WlLevel& L0, const WlLevel& L1, unsigned*
                                  cudaStream_t stream);
 
 void wl_count_launch();
+// Diagnostic per-CTA timestamps (WL_DIAG_TIMES builds; wl_diag_set)
+unsigned long long* wl_diag_ptr();
 // Records `msg` as this thread's wl_last_error() and returns `code`.
 int wl_fail(int code, const char* msg);
 

@@ -9,7 +9,11 @@ import os
 import statistics
 import sys
 
-import torch
+# several builds of the same kernels in one process: load every module eagerly
+# (with lazy loading a launch of one build's kernel can resolve to another's,
+# whose large-shared-memory attribute was never set -> "invalid argument")
+os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
+import torch  # noqa: E402
 
 SCHEMES = ["sweldens", "iwahashi", "iwahashi_star", "explosive", "explosive_star",
            "monolithic", "monolithic_star", "polyphase", "polyphase_star", "convolution"]
@@ -19,11 +23,13 @@ n = int(sys.argv[1])
 tags = sys.argv[2].split(",")
 G = int(os.environ.get("G", "10"))
 ROUNDS = int(os.environ.get("ROUNDS", "7"))
+SLEEP = int(os.environ.get("SLEEP", "4000000"))
 P, I, L = ctypes.c_void_p, ctypes.c_int, ctypes.c_long
 libs = []
 for t in tags:
     path = os.path.join(PKG, "libwavelift_b200.so" if t == "base" else f"libwavelift_b200_{t}.so")
-    lib = ctypes.CDLL(path)
+    lib = ctypes.CDLL(os.environ.get("WL_LIB_" + t, path))
+    lib.wl_last_error.restype = ctypes.c_char_p
     lib.wl_dwt2_forward.argtypes = [P, I, I, L, I, I, I, I, P, P, P, P, L, P]
     lib.wl_dwt2_inverse.argtypes = [P, P, P, P, I, I, L, I, I, I, I, P, L, P]
     libs.append(lib)
@@ -46,13 +52,15 @@ for prog in sys.argv[3:]:
                                        q[3].data_ptr(), n // 2, n // 2, n // 2, wi, si, 0, 0,
                                        rec.data_ptr(), n, None)
         res = {t: [] for t in tags}
-        for lib in libs:
+        for t, lib in zip(tags, libs):
             for _ in range(3):
-                assert call(lib) == 0
+                rc = call(lib)
+                assert rc == 0, (t, prog, d, rc, lib.wl_last_error())
         for _ in range(ROUNDS):
             for t, lib in zip(tags, libs):
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 call(lib)
+                torch.cuda._sleep(SLEEP)  # enqueue the group while the GPU sleeps
                 e0.record()
                 for _ in range(G):
                     call(lib)
