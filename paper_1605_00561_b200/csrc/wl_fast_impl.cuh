@@ -434,37 +434,56 @@ struct Acc {
     }
 };
 
-// Packed pair of cells (CC, CC + S) of row RR for the FFMA2 neighbour code
-// (P::nbr2): both cells run the scalar code's operation sequence, one packed
-// instruction per tap for the two of them.
-template <int R, int CPT, int RR, int CC, int S>
-struct Acc2 {
-    Acc<R, CPT, RR, CC> a0;
-    Acc<R, CPT, RR, CC + S> a1;
+// Pair mode (FP32-issue-bound programs, CPT = 4): the lane's four cells of a
+// row are held as two packed pairs A = (c0, c2), B = (c1, c3) and every tap
+// of P::nbr2 is ONE packed FFMA2 for two cells (same per-cell operation
+// sequence as the scalar code). Horizontal neighbours of a pair are the
+// pairs L = (c-1, c1) and Rt = (c2, c4) (c-1 / c4 from the adjacent lanes),
+// built once per row and epoch. Output pair PP (0 = A, 1 = B) of block row
+// RR reads position k = PP + DC in {L, A, B, Rt} of block row RR + DR
+// (-1 = the ghost row above, R = below); lt / rt hold L / Rt per block row.
+template <int R, int RR, int PP>
+struct AccP {
+    const wl2 (&v2)[R][2][4];
+    const wl2 (&gu2)[2][4];
+    const wl2 (&gd2)[2][4];
+    const wl2 (&lt)[R + 2][4];
+    const wl2 (&rt)[R + 2][4];
     template <int C, int DR, int DC>
     __device__ __forceinline__ wl2 g() const {
-        return wl_pk(a0.template g<C, DR, DC>(), a1.template g<C, DR, DC>());
+        constexpr int r = RR + DR, k = PP + DC;
+        if constexpr (k < 0)
+            return lt[r + 1][C];
+        else if constexpr (k > 1)
+            return rt[r + 1][C];
+        else if constexpr (r < 0)
+            return gu2[k][C];
+        else if constexpr (r >= R)
+            return gd2[k][C];
+        else
+            return v2[r][k][C];
     }
 };
-// Pair stride per program (0 = scalar FFMA code). FP32-issue-bound programs
-// (cdf97 Polyphase: 126 MACs per cell) issue half the FMA instructions packed.
+// Programs that may run in pair mode: the cdf97 Polyphase forward and inverse
+// (126 MACs per cell in two neighbour epochs, no local steps). Measured OFF
+// (profiles/tuning_r02_s2.txt): 24% fewer instructions, but 4% slower at
+// 8192^2 (0.165 vs 0.158 ms; stalls move to fixed-latency dependencies of
+// the half as many, twice as wide accumulation chains) -- the kernel is not
+// issue-bound. WL_PAIR_POLY=1 turns it on (A/B knob).
 #ifndef WL_PAIR_POLY
 #define WL_PAIR_POLY 0
 #endif
-#ifndef WL_PAIR_ALL
-#define WL_PAIR_ALL 0
-#endif
 template <class P>
-struct PairStride {
-    static constexpr int S = WL_PAIR_ALL;
+struct PairMode {
+    static constexpr bool on = false;
 };
 template <>
-struct PairStride<P_cdf97_polyphase_fwd> {
-    static constexpr int S = WL_PAIR_POLY;
+struct PairMode<P_cdf97_polyphase_fwd> {
+    static constexpr bool on = WL_PAIR_POLY;
 };
 template <>
-struct PairStride<P_cdf97_polyphase_inv> {
-    static constexpr int S = WL_PAIR_POLY;
+struct PairMode<P_cdf97_polyphase_inv> {
+    static constexpr bool on = WL_PAIR_POLY;
 };
 
 // kUse bit layout (gen_steps.py usage_mask): comp*9 + (dr+1)*3 + (dc+1).
@@ -1050,6 +1069,23 @@ __global__ void __launch_bounds__((NW + 1) * 32,
                 for (int r = 0; r < R; ++r) P::pre(v[r][c]);
             }
 
+            // pair mode: the state as packed pairs A = (c0, c2), B = (c1, c3)
+            constexpr bool PM = PairMode<P>::on && CPT == 4 && !MIRROR && !FUSED;
+            wl2 v2[PM ? R : 1][2][4], gu2[2][4], gd2[2][4];
+            if constexpr (PM) {
+                auto pack = [&](const float (&src)[CPT][4], wl2 (&dst)[2][4]) {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        dst[0][k] = wl_pk_keep(src[0][k], src[2][k]);
+                        dst[1][k] = wl_pk_keep(src[1][k], src[3][k]);
+                    }
+                };
+                pack(gu, gu2);
+                pack(gd, gd2);
+#pragma unroll
+                for (int r = 0; r < R; ++r) pack(v[r], v2[r < (PM ? R : 1) ? r : 0]);
+            }
+
 #ifndef WL_DIAG_NO_COMPUTE
             sfor<P::kEpochs>([&](auto e_) {
                 constexpr int E = decltype(e_)::value;
@@ -1084,6 +1120,88 @@ __global__ void __launch_bounds__((NW + 1) * 32,
                         row[0][C] = q.x; row[1][C] = q.y;
                     }
                 };
+                if constexpr (PM) {
+                    // ---- pair mode: exchange, then rows top to bottom with a
+                    // sliding window of L / Rt pairs (one output row's delay
+                    // before it replaces its input row)
+                    if constexpr (E > 0) {
+                        sfor<4>([&](auto c_) {
+                            constexpr int C = decltype(c_)::value;
+                            if constexpr (xch_up(U, C, XF))
+                                reinterpret_cast<ulonglong2*>(xw + xch_rank(U, C, -1, XF) * kCompF)[lane] =
+                                    make_ulonglong2(v2[R - 1][0][C], v2[R - 1][1][C]);
+                            if constexpr (xch_dn(U, C, XF))
+                                reinterpret_cast<ulonglong2*>(xw + (NUP + xch_rank(U, C, 1, XF)) * kCompF)[lane] =
+                                    make_ulonglong2(v2[0][0][C], v2[0][1][C]);
+                        });
+                        named_sync(1, NW * 32);  // the epoch's block barrier
+                        sfor<4>([&](auto c_) {
+                            constexpr int C = decltype(c_)::value;
+                            if constexpr (xch_up(U, C, XF))
+                                if (warp > 0) {
+                                    const ulonglong2 q = reinterpret_cast<const ulonglong2*>(
+                                        xw - kSlotF + xch_rank(U, C, -1, XF) * kCompF)[lane];
+                                    gu2[0][C] = q.x;
+                                    gu2[1][C] = q.y;
+                                }
+                            if constexpr (xch_dn(U, C, XF))
+                                if (warp < NW - 1) {
+                                    const ulonglong2 q = reinterpret_cast<const ulonglong2*>(
+                                        xw + kSlotF + (NUP + xch_rank(U, C, 1, XF)) * kCompF)[lane];
+                                    gd2[0][C] = q.x;
+                                    gd2[1][C] = q.y;
+                                }
+                        });
+                        xslot ^= 1;
+                    }
+                    wl2 lt[R + 2][4], rt[R + 2][4];
+                    // L / Rt pairs of block row T - 1 (0 = ghost row above)
+                    auto lr = [&](auto t_) {
+                        constexpr int T = decltype(t_)::value - 1;
+                        const wl2 (&rw)[2][4] =
+                            T < 0 ? gu2 : (T >= R ? gd2 : v2[T < 0 ? 0 : (T >= R ? R - 1 : T)]);
+                        sfor<4>([&](auto c_) {
+                            constexpr int C = decltype(c_)::value;
+                            constexpr bool nl = T < 0 ? uses(U, C, -1, -1)
+                                                      : (T >= R ? uses(U, C, 1, -1) : uses_dc(U, C, -1));
+                            constexpr bool nr = T < 0 ? uses(U, C, -1, 1)
+                                                      : (T >= R ? uses(U, C, 1, 1) : uses_dc(U, C, 1));
+                            if constexpr (nl) {
+                                const float c3 = __shfl_up_sync(0xffffffffu, wl_hi(rw[1][C]), 1);
+                                lt[T + 1][C] = wl_pk_keep(c3, wl_lo(rw[1][C]));
+                            }
+                            if constexpr (nr) {
+                                const float c4 = __shfl_down_sync(0xffffffffu, wl_lo(rw[0][C]), 1);
+                                rt[T + 1][C] = wl_pk_keep(wl_hi(rw[0][C]), c4);
+                            }
+                        });
+                    };
+                    wl2 o2[R][2][4];
+                    lr(std::integral_constant<int, 0>{});
+                    lr(std::integral_constant<int, 1>{});
+                    sfor<R>([&](auto r_) {
+                        constexpr int RR = decltype(r_)::value;
+                        lr(std::integral_constant<int, RR + 2>{});
+                        sfor<2>([&](auto p_) {
+                            AccP<R, RR, decltype(p_)::value> acc{v2, gu2, gd2, lt, rt};
+                            P::template nbr2<E>(acc, o2[RR][decltype(p_)::value]);
+                        });
+                        if constexpr (RR >= 1) {
+#pragma unroll
+                            for (int k = 0; k < 4; ++k) {
+                                v2[RR - 1][0][k] = o2[RR - 1][0][k];
+                                v2[RR - 1][1][k] = o2[RR - 1][1][k];
+                            }
+                        }
+                    });
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        v2[R - 1][0][k] = o2[R - 1][0][k];
+                        v2[R - 1][1][k] = o2[R - 1][1][k];
+                    }
+                    (void)NDN;
+                    return;
+                }
                 if constexpr (E > 0) {
                     sfor<4>([&](auto c_) {
                         constexpr int C = decltype(c_)::value;
@@ -1178,29 +1296,13 @@ __global__ void __launch_bounds__((NW + 1) * 32,
                 });
                 if constexpr (MIRROR) hfix(sl, sr, 1, R);
                 float o[R][CPT][4];
-                constexpr int PS = PairStride<P>::S < CPT ? PairStride<P>::S : 0;
                 auto row = [&](auto r_) {
                     constexpr int RR = decltype(r_)::value;
-                    if constexpr (PS > 0) {
-                        sfor<CPT / 2>([&](auto p_) {
-                            constexpr int p = decltype(p_)::value;
-                            constexpr int C0 = (p / PS) * 2 * PS + p % PS, C1 = C0 + PS;
-                            Acc2<R, CPT, RR, C0, PS> acc{{v, gu, gd, sl, sr}, {v, gu, gd, sl, sr}};
-                            wl2 o2[4];
-                            P::template nbr2<E>(acc, o2);
-#pragma unroll
-                            for (int k = 0; k < 4; ++k) {
-                                o[RR][C0][k] = wl_lo(o2[k]);
-                                o[RR][C1][k] = wl_hi(o2[k]);
-                            }
-                        });
-                    } else {
-                        sfor<CPT>([&](auto c_) {
-                            constexpr int CC = decltype(c_)::value;
-                            Acc<R, CPT, RR, CC> acc{v, gu, gd, sl, sr};
-                            P::template nbr<E>(acc, o[RR][CC]);
-                        });
-                    }
+                    sfor<CPT>([&](auto c_) {
+                        constexpr int CC = decltype(c_)::value;
+                        Acc<R, CPT, RR, CC> acc{v, gu, gd, sl, sr};
+                        P::template nbr<E>(acc, o[RR][CC]);
+                    });
                 };
                 // interior rows 1..R-2 read only this warp's rows
                 sfor<R - 2>([&](auto r_) { row(std::integral_constant<int, decltype(r_)::value + 1>{}); });
@@ -1241,6 +1343,17 @@ __global__ void __launch_bounds__((NW + 1) * 32,
                     }
             });
 
+            if constexpr (PM) {
+#pragma unroll
+                for (int r = 0; r < R; ++r)
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        v[r][0][k] = wl_lo(v2[r < (PM ? R : 1) ? r : 0][0][k]);
+                        v[r][2][k] = wl_hi(v2[r < (PM ? R : 1) ? r : 0][0][k]);
+                        v[r][1][k] = wl_lo(v2[r < (PM ? R : 1) ? r : 0][1][k]);
+                        v[r][3][k] = wl_hi(v2[r < (PM ? R : 1) ? r : 0][1][k]);
+                    }
+            }
 #endif  // WL_DIAG_NO_COMPUTE
             // ---------------- store ----------------
             const int gy0 = cy + 1 + warp * R;  // global cell row of v[0]
