@@ -164,6 +164,9 @@ def barrier(ws):
 PROGRAMS = [(w, s) for w in WAVELETS for s in SCHEMES]
 # the reference CPU timed at the full configs[1] size (the headline pair)
 CPU_FULL = (("cdf53", "monolithic"), ("cdf97", "monolithic_star"))
+# dd137 schemes on the fast engine (Polyphase(*) of reach 3 stay on the interpreter)
+DD137_FAST = ("sweldens", "iwahashi", "iwahashi_star", "explosive", "explosive_star",
+              "monolithic", "monolithic_star")
 # configs[2] ablation at 16384^2: the north-star kernels and their neighbours
 C3_PROGRAMS = (("cdf97", "monolithic_star"), ("cdf97", "monolithic"), ("cdf97", "sweldens"),
                ("cdf53", "monolithic"), ("cdf53", "monolithic_star"))
@@ -430,6 +433,27 @@ def run_gpu(args):
                 unaligned["8190/cdf97/monolithic_star/fwd/interpreter"] = prog_entry(t, m, peak)
             del im, qm, rm
 
+    # ---- dd137: the fast engine's reach-2 kernels for every
+    # lifting scheme but Polyphase(*) (interpreter), 8192^2, same image; the
+    # generic interpreter on one scheme for scale
+    dd = None
+    if args.dd137 and ws == 1:
+        dd = {}
+        for s in DD137_FAST:
+            sch = wl.build_scheme(s, "dd137")
+            tf = time_isolated(lambda: wl.forward(img, sch, out=q), stream)
+            ti = time_isolated(lambda: wl.inverse(q, "dd137", scheme=s, out=rec), stream)
+            dd[f"dd137/{s}/fwd"] = prog_entry(tf, n, peak)
+            dd[f"dd137/{s}/inv"] = prog_entry(ti, n, peak)
+        prev = wl.set_engine(1)
+        sch = wl.build_scheme("monolithic_star", "dd137")
+        t = time_isolated(lambda: wl.forward(img, sch, out=q), stream, groups=3, per_group=3)
+        wl.set_engine(prev)
+        dd["dd137/monolithic_star/fwd/interpreter"] = prog_entry(t, n, peak)
+        sch = wl.build_scheme("polyphase", "dd137")
+        t = time_isolated(lambda: wl.forward(img, sch, out=q), stream, groups=3, per_group=3)
+        dd["dd137/polyphase/fwd/interpreter"] = prog_entry(t, n, peak)
+
     # ---- e2e through the public API with pinned host buffers
     e2e = None
     if args.e2e_steps > 0:
@@ -451,11 +475,11 @@ def run_gpu(args):
                 "config": workload_config(n, ws),
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches, "gpu_launches_per_step": launches / args.steps,
-                "clocks": clocks, "c4": c4, "c5": c5, "unaligned": unaligned,
+                "clocks": clocks, "c4": c4, "c5": c5, "unaligned": unaligned, "dd137": dd,
                 "per_scheme_unit": "[ms, GPix/s, frac of copy peak] per launch, isolated steady "
                                    "state (median of 5 groups of 10 back-to-back launches)",
                 "per_scheme": per,
-                "north_star": north_star(c3, c4, c5, unaligned)}
+                "north_star": north_star(c3, c4, c5, unaligned, dd)}
         print(json.dumps(line), flush=True)
     if ws > 1:
         import torch.distributed as dist
@@ -463,9 +487,12 @@ def run_gpu(args):
     return 0
 
 
-def north_star(c3, c4, c5, unaligned=None):
+def north_star(c3, c4, c5, unaligned=None, dd=None):
     """Compact configs[2..4] summary, emitted LAST in the line."""
     out = {}
+    if dd:
+        out["dd137_unit"] = "8192^2: [ms, frac of copy peak]"
+        out["dd137"] = {k: [v["ms"], v["frac"]] for k, v in dd.items()}
     if unaligned:
         out["unaligned_unit"] = "[ms, frac of copy peak] (8190^2 / 8194^2 images: no TMA)"
         out["unaligned"] = {k: [v["ms"], v["frac"]] for k, v in unaligned.items()}
@@ -749,6 +776,7 @@ def main():
     ap.add_argument("--c5-pool", type=int, default=256)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-unaligned", dest="unaligned", action="store_false")
+    ap.add_argument("--no-dd137", dest="dd137", action="store_false")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

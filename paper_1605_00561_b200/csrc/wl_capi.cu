@@ -81,8 +81,8 @@ int launch_level_batch(WlLevel L, cudaStream_t s) {
     }
     const WlProgram& P = wl_host_program(Lp.prog);
     const int engine = g_engine.load();
-    const bool batched = engine != 1 && Lp.wavelet <= 1 &&
-                         (P.is_conv ? (L.in_bstride[0] % 4 == 0) : wl_fast_supported(Lp));
+    const bool batched = engine != 1 && (P.is_conv ? (Lp.wavelet <= 1 && L.in_bstride[0] % 4 == 0)
+                                                   : wl_fast_supported(Lp));
     if (batched) return launch_level(L, s);
     for (int b = 0; b < L.nb; ++b) {
         WlLevel Li = L;

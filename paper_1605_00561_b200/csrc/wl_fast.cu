@@ -102,6 +102,12 @@ cudaError_t wl_fast_cdf53_direct(int scheme, const WlLevel& L, const wlfast::Pla
                                  cudaStream_t s);
 cudaError_t wl_fast_cdf97_direct(int scheme, const WlLevel& L, const wlfast::Plan& p,
                                  cudaStream_t s);
+cudaError_t wl_fast_dd137_fwd(int scheme, const WlLevel& L, const wlfast::Plan& p,
+                              cudaStream_t s);
+cudaError_t wl_fast_dd137_inv(int scheme, const WlLevel& L, const wlfast::Plan& p,
+                              cudaStream_t s);
+cudaError_t wl_fast_dd137_direct(int scheme, const WlLevel& L, const wlfast::Plan& p,
+                                 cudaStream_t s);
 cudaError_t wl_fast_cdf53_fwd_fused(int scheme, const WlLevel& L0, const wlfast::Plan& p0,
                                    const WlLevel& L1, const wlfast::Plan& p1, unsigned* ctr,
                                    cudaStream_t s);
@@ -112,35 +118,46 @@ cudaError_t wl_fast_cdf97_fwd_fused(int scheme, const WlLevel& L0, const wlfast:
 namespace {
 
 template <class C>
-void geo(int* R, int* NW, int* CPT) {
+void geo(int* R, int* NW, int* CPT, int* KR) {
     *R = C::R;
     *NW = C::NW;
     *CPT = C::CPT;
+    *KR = C::KR;
 }
 
 // Tile geometry of the instantiation that serves (wavelet, scheme, direction)
 // -- must match the SchemeConfig the kernel was compiled with.
 template <int W, int D>
-void geo_wd(int scheme, int* R, int* NW, int* CPT) {
+void geo_wd(int scheme, int* R, int* NW, int* CPT, int* KR) {
     using namespace wlfast;
     switch (scheme) {
-        case 0: return geo<SchemeConfig<W, D, 0>>(R, NW, CPT);
-        case 1: return geo<SchemeConfig<W, D, 1>>(R, NW, CPT);
-        case 2: return geo<SchemeConfig<W, D, 2>>(R, NW, CPT);
-        case 3: return geo<SchemeConfig<W, D, 3>>(R, NW, CPT);
-        case 4: return geo<SchemeConfig<W, D, 4>>(R, NW, CPT);
-        case 5: return geo<SchemeConfig<W, D, 5>>(R, NW, CPT);
-        case 6: return geo<SchemeConfig<W, D, 6>>(R, NW, CPT);
-        case 7: return geo<SchemeConfig<W, D, 7>>(R, NW, CPT);
-        default: return geo<SchemeConfig<W, D, 8>>(R, NW, CPT);
+        case 0: return geo<SchemeConfig<W, D, 0>>(R, NW, CPT, KR);
+        case 1: return geo<SchemeConfig<W, D, 1>>(R, NW, CPT, KR);
+        case 2: return geo<SchemeConfig<W, D, 2>>(R, NW, CPT, KR);
+        case 3: return geo<SchemeConfig<W, D, 3>>(R, NW, CPT, KR);
+        case 4: return geo<SchemeConfig<W, D, 4>>(R, NW, CPT, KR);
+        case 5: return geo<SchemeConfig<W, D, 5>>(R, NW, CPT, KR);
+        case 6: return geo<SchemeConfig<W, D, 6>>(R, NW, CPT, KR);
+        case 7: return geo<SchemeConfig<W, D, 7>>(R, NW, CPT, KR);
+        default: return geo<SchemeConfig<W, D, 8>>(R, NW, CPT, KR);
     }
 }
 
-void geometry(const WlLevel& L, int* R, int* NW, int* CPT) {
+void geometry(const WlLevel& L, int* R, int* NW, int* CPT, int* KR) {
+    const bool f = L.direction == 0;
     if (L.wavelet == 0)
-        L.direction == 0 ? geo_wd<0, 0>(L.scheme, R, NW, CPT) : geo_wd<0, 1>(L.scheme, R, NW, CPT);
+        f ? geo_wd<0, 0>(L.scheme, R, NW, CPT, KR) : geo_wd<0, 1>(L.scheme, R, NW, CPT, KR);
+    else if (L.wavelet == 1)
+        f ? geo_wd<1, 0>(L.scheme, R, NW, CPT, KR) : geo_wd<1, 1>(L.scheme, R, NW, CPT, KR);
     else
-        L.direction == 0 ? geo_wd<1, 0>(L.scheme, R, NW, CPT) : geo_wd<1, 1>(L.scheme, R, NW, CPT);
+        f ? geo_wd<2, 0>(L.scheme, R, NW, CPT, KR) : geo_wd<2, 1>(L.scheme, R, NW, CPT, KR);
+}
+
+// Programs the fast engine serves: cdf53 / cdf97 lifting schemes, and the
+// dd137 lifting schemes except Polyphase(*) (reach 3, interpreter).
+bool fast_program(int wavelet, int scheme) {
+    if (wavelet < 0 || wavelet > 2 || scheme < 0 || scheme > 8) return false;
+    return wavelet < 2 || scheme <= 6;
 }
 
 bool aligned(const void* p, int bytes) { return (reinterpret_cast<uintptr_t>(p) % bytes) == 0; }
@@ -193,13 +210,14 @@ bool direct_ok(const WlLevel& L) {
 }  // namespace
 
 int wl_fast_mode(const WlLevel& L) {
-    if (L.wavelet < 0 || L.wavelet > 1 || L.scheme < 0 || L.scheme > 8) return 0;
-    int R, NW, CPT;
-    geometry(L, &R, &NW, &CPT);
+    if (!fast_program(L.wavelet, L.scheme)) return 0;
+    int R, NW, CPT, KR;
+    geometry(L, &R, &NW, &CPT, &KR);
     const int H = wl_host_program(L.prog).halo;
     const bool force_direct = wl_engine() == 3;
-    if (!force_direct && tma_ok(L, CPT) && wlfast::plan_tiles(L, H, R, NW, CPT).ok) return 1;
-    if (direct_ok(L) && wlfast::plan_tiles(L, H, R, NW, CPT, true).ok) return 2;
+    if (!force_direct && tma_ok(L, CPT) && wlfast::plan_tiles(L, H, R, NW, CPT, false, false, KR).ok)
+        return 1;
+    if (direct_ok(L) && wlfast::plan_tiles(L, H, R, NW, CPT, true, false, KR).ok) return 2;
     return 0;
 }
 
@@ -208,20 +226,24 @@ bool wl_fast_supported(const WlLevel& L) { return wl_fast_mode(L) != 0; }
 cudaError_t wl_launch_fast(const WlLevel& L, cudaStream_t stream) {
     const int mode = wl_fast_mode(L);
     if (!mode) return cudaErrorNotSupported;
-    int R, NW, CPT;
-    geometry(L, &R, &NW, &CPT);
+    int R, NW, CPT, KR;
+    geometry(L, &R, &NW, &CPT, &KR);
     const int H = wl_host_program(L.prog).halo;
-    const wlfast::Plan plan = wlfast::plan_tiles(L, H, R, NW, CPT, mode == 2);
+    const wlfast::Plan plan = wlfast::plan_tiles(L, H, R, NW, CPT, mode == 2, false, KR);
     cudaError_t e;
     if (mode == 2)
-        e = L.wavelet == 0 ? wl_fast_cdf53_direct(L.scheme, L, plan, stream)
-                           : wl_fast_cdf97_direct(L.scheme, L, plan, stream);
+        e = L.wavelet == 0   ? wl_fast_cdf53_direct(L.scheme, L, plan, stream)
+            : L.wavelet == 1 ? wl_fast_cdf97_direct(L.scheme, L, plan, stream)
+                             : wl_fast_dd137_direct(L.scheme, L, plan, stream);
     else if (L.wavelet == 0)
         e = L.direction == 0 ? wl_fast_cdf53_fwd(L.scheme, L, plan, stream)
                              : wl_fast_cdf53_inv(L.scheme, L, plan, stream);
-    else
+    else if (L.wavelet == 1)
         e = L.direction == 0 ? wl_fast_cdf97_fwd(L.scheme, L, plan, stream)
                              : wl_fast_cdf97_inv(L.scheme, L, plan, stream);
+    else
+        e = L.direction == 0 ? wl_fast_dd137_fwd(L.scheme, L, plan, stream)
+                             : wl_fast_dd137_inv(L.scheme, L, plan, stream);
     if (e != cudaSuccess) return e;
     // periodic, or symmetric with mirrored border tiles: the grid covers the image
     if (plan.args.wrap || plan.args.mirror) return cudaSuccess;
@@ -275,10 +297,10 @@ cudaError_t wl_launch_fast_fused(const WlLevel& L0, const WlLevel& L1, unsigned*
         L0.nb != L1.nb || L1.qw * 2 != L0.qw || L1.qh * 2 != L0.qh || L1.in[0] != L0.out[0] ||
         L1.in_pitch != L0.out_pitch || (L0.nb > 1 && L1.in_bstride[0] != L0.out_bstride[0]))
         return cudaErrorNotSupported;
-    if (wl_host_program(L0.prog).is_conv) return cudaErrorNotSupported;
+    if (wl_host_program(L0.prog).is_conv || L0.wavelet > 1) return cudaErrorNotSupported;
     if (wl_fast_mode(L0) != 1 || wl_fast_mode(L1) != 1) return cudaErrorNotSupported;
-    int R, NW, CPT;
-    geometry(L0, &R, &NW, &CPT);
+    int R, NW, CPT, KR;
+    geometry(L0, &R, &NW, &CPT, &KR);
     const int H = wl_host_program(L0.prog).halo;
     const wlfast::Plan p0 = wlfast::plan_tiles(L0, H, R, NW, CPT, false, true);
     const wlfast::Plan p1 = wlfast::plan_tiles(L1, H, R, NW, CPT, false, true);

@@ -1,0 +1,29 @@
+// Instantiation unit of the fast engine: dd137, direct-load variant (no TMA;
+// wlfast::launch_direct), both directions, lifting schemes except Polyphase(*) (reach 3: interpreter).
+#include "wl_fast_impl.cuh"
+
+cudaError_t wl_fast_dd137_direct(int scheme, const WlLevel& L, const wlfast::Plan& p,
+                               cudaStream_t s) {
+#define WL_CASE(wi, si, d, P)                                                               \
+    case si:                                                                                \
+        static_assert(P::kReach == wlfast::SchemeConfig<wi, d, si>::KR, "reach");           \
+        return wlfast::launch_direct<P, d, wlfast::SchemeConfig<wi, d, si>::R,              \
+                                     wlfast::SchemeConfig<wi, d, si>::NW,                   \
+                                     wlfast::SchemeConfig<wi, d, si>::CPT,                  \
+                                     wlfast::SchemeConfig<wi, d, si>::NS,                   \
+                                     wlfast::SchemeConfig<wi, d, si>::XF,                   \
+                                     wlfast::SchemeConfig<wi, d, si>::MAXB>(L, p, s);
+    if (L.direction == 0) {
+        switch (scheme) {
+            WL_FAST_FOREACH_2_0(WL_CASE)
+            default:
+                return cudaErrorNotSupported;
+        }
+    }
+    switch (scheme) {
+        WL_FAST_FOREACH_2_1(WL_CASE)
+        default:
+            return cudaErrorNotSupported;
+    }
+#undef WL_CASE
+}

@@ -394,15 +394,15 @@ struct ProdBackoff<P_cdf97_polyphase_inv, 1> {
     static constexpr int ns = WL_PROD_BACKOFF_NS;
 };
 
-template <int R, int NW, int CPT, int NS = 2, int NXC = 4>
+template <int R, int NW, int CPT, int NS = 2, int NXC = 4, int KR = 1>
 struct Geometry {
     static constexpr int kStages = NS;                       // TMA ring depth
     static constexpr int TWC = 32 * CPT;                     // compute-region width in cells
-    static constexpr int kRows = NW * R + 2;                 // cell rows per stage incl. ghosts
+    static constexpr int kRows = NW * R + 2 * KR;            // cell rows per stage incl. KR ghosts
     static constexpr int kStageFloats = 4 * TWC * kRows;     // == 2*TWC px * 2*kRows px
     static constexpr int kStageBytes = kStageFloats * 4;
     // edge exchange: 2 slots x NW warps x NXC published component rows of
-    // 32 * CPT cells (NXC = the most components any epoch reads across warps)
+    // 32 * CPT cells (NXC = the most component rows any epoch reads across warps)
     static constexpr int kXchFloats = 2 * NW * (NXC > WL_XCH_MIN ? NXC : WL_XCH_MIN) * 32 * CPT;
     static constexpr size_t kSmemBytes =
         NS * (size_t)kStageBytes + (size_t)kXchFloats * 4 + 16 * NS;
@@ -410,25 +410,28 @@ struct Geometry {
     static constexpr int kMinBlocks = 2 * (kSmemBytes + 1024) <= 233472 ? 2 : 1;
 };
 
-// Neighbour accessor for the cell at (row RR, column CC) of the lane's block.
-template <int R, int CPT, int RR, int CC>
+// Neighbour accessor for the cell at (row RR, column CC) of the lane's block:
+// KR ghost rows above (gu[0] = row -KR) and below (gd[0] = row R), and per
+// block row KR cells left (sl[.][j] = column -1-j) / right (sr[.][j] = column
+// CPT+j) from the adjacent lanes; sl/sr rows are indexed block row + KR.
+template <int R, int CPT, int KR, int RR, int CC>
 struct Acc {
     const float (&v)[R][CPT][4];
-    const float (&gu)[CPT][4];
-    const float (&gd)[CPT][4];
-    const float (&sl)[R + 2][4];
-    const float (&sr)[R + 2][4];
+    const float (&gu)[KR][CPT][4];
+    const float (&gd)[KR][CPT][4];
+    const float (&sl)[R + 2 * KR][KR][4];
+    const float (&sr)[R + 2 * KR][KR][4];
     template <int C, int DR, int DC>
     __device__ __forceinline__ float g() const {
         constexpr int r = RR + DR, c = CC + DC;
         if constexpr (c < 0)
-            return sl[r + 1][C];
+            return sl[r + KR][-c - 1][C];
         else if constexpr (c >= CPT)
-            return sr[r + 1][C];
+            return sr[r + KR][c - CPT][C];
         else if constexpr (r < 0)
-            return gu[c][C];
+            return gu[r + KR][c][C];
         else if constexpr (r >= R)
-            return gd[c][C];
+            return gd[r - R][c][C];
         else
             return v[r][c][C];
     }
@@ -486,53 +489,103 @@ struct PairMode<P_cdf97_polyphase_inv> {
     static constexpr bool on = WL_PAIR_POLY;
 };
 
-// kUse bit layout (gen_steps.py usage_mask): comp*9 + (dr+1)*3 + (dc+1).
-__host__ __device__ constexpr bool uses(unsigned long long m, int c, int dr, int dc) {
-    return (m >> (c * 9 + (dr + 1) * 3 + (dc + 1))) & 1ull;
+// Neighbour reads of one epoch (gen_steps.py usage_masks): per source
+// component c, bit (dr + k) * (2k + 1) + (dc + k) for every tap offset, k =
+// the program's reach (P::kReach: 1 for cdf53 / cdf97, 2 for dd137).
+struct UseT {
+    unsigned long long m[4];
+    int k;
+};
+template <class P, int E>
+__host__ __device__ constexpr UseT use_of() {
+    return UseT{{P::kUse[E][0], P::kUse[E][1], P::kUse[E][2], P::kUse[E][3]}, P::kReach};
 }
-__host__ __device__ constexpr bool uses_dc(unsigned long long m, int c, int dc) {
-    return uses(m, c, -1, dc) || uses(m, c, 0, dc) || uses(m, c, 1, dc);
+__host__ __device__ constexpr bool uses(const UseT& u, int c, int dr, int dc) {
+    if (dr < -u.k || dr > u.k || dc < -u.k || dc > u.k) return false;
+    return (u.m[c] >> ((dr + u.k) * (2 * u.k + 1) + (dc + u.k))) & 1ull;
 }
-__host__ __device__ constexpr bool uses_dr(unsigned long long m, int c, int dr) {
-    return uses(m, c, dr, -1) || uses(m, c, dr, 0) || uses(m, c, dr, 1);
+__host__ __device__ constexpr bool uses_dc(const UseT& u, int c, int dc) {
+    for (int dr = -u.k; dr <= u.k; ++dr)
+        if (uses(u, c, dr, dc)) return true;
+    return false;
 }
-// number of components read from the row above (dr = -1) / below (dr = +1)
-__host__ __device__ constexpr int n_dr(unsigned long long m, int dr) {
-    int n = 0;
-    for (int c = 0; c < 4; ++c) n += uses_dr(m, c, dr) ? 1 : 0;
-    return n;
+__host__ __device__ constexpr bool uses_dr(const UseT& u, int c, int dr) {
+    for (int dc = -u.k; dc <= u.k; ++dc)
+        if (uses(u, c, dr, dc)) return true;
+    return false;
+}
+// Is cell (block row r, lane-relative column c) of component C read by any
+// of the lane's R x CPT cells? (r in [-k, R + k), c in [-k, CPT + k))
+__host__ __device__ constexpr bool reads(const UseT& u, int C, int r, int c, int R, int CPT) {
+    for (int t = 0; t < R; ++t)
+        for (int cc = 0; cc < CPT; ++cc)
+            if (uses(u, C, r - t, c - cc)) return true;
+    return false;
 }
 // Exchange mode: minimal (publish only the component rows the neighbour
 // warps read this epoch: a lifting epoch reads across warps from one side
-// only, 2 components; Polyphase up to 6) or full (both edge rows, all 4
-// components). Chosen per configuration by measurement (Config::kFullXch).
-// Exchange mode: minimal (publish only the component rows the neighbour
-// warps read this epoch: a lifting epoch reads across warps from one side
-// only, 2 components; Polyphase up to 6) or full (both edge rows, all 4
-// components). Chosen per configuration by measurement (Config::kFullXch).
-__host__ __device__ constexpr bool xch_up(unsigned long long m, int c, bool full) {
-    return full || uses_dr(m, c, -1);
+// only, 2 components; Polyphase up to 6) or full (the k edge rows on both
+// sides, all 4 components). Chosen per configuration by measurement
+// (Config::XF). xch_up / xch_dn = rows of component c published for the warp
+// below / above: rows R-1..R-n / 0..n-1 of this warp, n = the deepest read.
+__host__ __device__ constexpr int xch_up(const UseT& u, int c, bool full) {
+    if (full) return u.k;
+    for (int n = u.k; n >= 1; --n)
+        if (uses_dr(u, c, -n)) return n;
+    return 0;
 }
-__host__ __device__ constexpr bool xch_dn(unsigned long long m, int c, bool full) {
-    return full || uses_dr(m, c, 1);
+__host__ __device__ constexpr int xch_dn(const UseT& u, int c, bool full) {
+    if (full) return u.k;
+    for (int n = u.k; n >= 1; --n)
+        if (uses_dr(u, c, n)) return n;
+    return 0;
 }
-__host__ __device__ constexpr int xch_rank(unsigned long long m, int c, int dr, bool full) {
+__host__ __device__ constexpr int xch_rank(const UseT& u, int c, int dr, bool full) {
     int n = 0;
-    for (int k = 0; k < c; ++k) n += (dr < 0 ? xch_up(m, k, full) : xch_dn(m, k, full)) ? 1 : 0;
+    for (int k = 0; k < c; ++k) n += dr < 0 ? xch_up(u, k, full) : xch_dn(u, k, full);
     return n;
 }
-__host__ __device__ constexpr int xch_count(unsigned long long m, int dr, bool full) {
-    return xch_rank(m, 4, dr, full);
+__host__ __device__ constexpr int xch_count(const UseT& u, int dr, bool full) {
+    return xch_rank(u, 4, dr, full);
 }
-template <class P, bool FULL>
+// The same queries through a tag type carrying the epoch's UseT as a static
+// member (usable inside the nested per-component lambdas of the kernel,
+// where a captured constexpr struct is not a constant expression).
+template <class P, int E>
+struct UseOf {
+    static constexpr UseT u = use_of<P, E>();
+};
+template <class UO, class = decltype(UO::u)>
+__host__ __device__ constexpr bool uses(UO, int c, int dr, int dc) { return uses(UO::u, c, dr, dc); }
+template <class UO, class = decltype(UO::u)>
+__host__ __device__ constexpr bool uses_dc(UO, int c, int dc) { return uses_dc(UO::u, c, dc); }
+template <class UO, class = decltype(UO::u)>
+__host__ __device__ constexpr bool uses_dr(UO, int c, int dr) { return uses_dr(UO::u, c, dr); }
+template <class UO, class = decltype(UO::u)>
+__host__ __device__ constexpr bool reads(UO, int C, int r, int c, int R, int CPT) {
+    return reads(UO::u, C, r, c, R, CPT);
+}
+template <class UO, class = decltype(UO::u)>
+__host__ __device__ constexpr int xch_up(UO, int c, bool full) { return xch_up(UO::u, c, full); }
+template <class UO, class = decltype(UO::u)>
+__host__ __device__ constexpr int xch_dn(UO, int c, bool full) { return xch_dn(UO::u, c, full); }
+template <class UO, class = decltype(UO::u)>
+__host__ __device__ constexpr int xch_rank(UO, int c, int dr, bool full) {
+    return xch_rank(UO::u, c, dr, full);
+}
+template <class UO, class = decltype(UO::u)>
+__host__ __device__ constexpr int xch_count(UO, int dr, bool full) { return xch_count(UO::u, dr, full); }
+
+template <class P, bool FULL, int E = 1>
 constexpr int xch_comps() {
-    if (FULL) return P::kEpochs > 1 ? 8 : 0;
-    int mx = 0;
-    for (int e = 1; e < P::kEpochs; ++e) {
-        const int n = n_dr(P::kUse[e], -1) + n_dr(P::kUse[e], 1);
-        mx = n > mx ? n : mx;
+    if constexpr (E >= P::kEpochs) {
+        return 0;
+    } else {
+        constexpr UseT u = use_of<P, E>();
+        constexpr int n = xch_count(u, -1, FULL) + xch_count(u, 1, FULL);
+        constexpr int rest = xch_comps<P, FULL, E + 1>();
+        return n > rest ? n : rest;
     }
-    return mx;
 }
 
 // DIRECT: no TMA -- shapes whose pitches/pointers/widths the TMA boxes and
@@ -544,7 +597,7 @@ constexpr int xch_comps() {
 template <class P, int DIR, int R, int NW, int CPT, int NS, bool XF, bool MIRROR,
           bool FUSED = false, bool DIRECT = false>
 __global__ void __launch_bounds__((NW + 1) * 32,
-                                  (Geometry<R, NW, CPT, NS, xch_comps<P, XF>()>::kMinBlocks))
+                                  (Geometry<R, NW, CPT, NS, xch_comps<P, XF>(), P::kReach>::kMinBlocks))
     fast_kernel(const __grid_constant__ CUtensorMap m0, const __grid_constant__ CUtensorMap m1,
                 const __grid_constant__ CUtensorMap m2, const __grid_constant__ CUtensorMap m3,
                 const __grid_constant__ KArgs K) {
@@ -557,7 +610,10 @@ __global__ void __launch_bounds__((NW + 1) * 32,
     __shared__ unsigned done_cnt[kRing];
     __shared__ int row_ring[kRing];
     constexpr int NXC = xch_comps<P, XF>();
-    using G = Geometry<R, NW, CPT, NS, NXC>;
+    constexpr int KR = P::kReach;  // ghost rows / neighbour cells a step reads
+    static_assert(R >= 2 * KR && KR <= CPT, "edge rows / lane-neighbour cells");
+    static_assert(KR == 1 || (!MIRROR && !FUSED), "reach-2 programs: plain / direct plans");
+    using G = Geometry<R, NW, CPT, NS, NXC, KR>;
     constexpr int H = P::kHalo;
     constexpr int TWC = G::TWC;
     constexpr int HX = halo_x<CPT, H>();
@@ -745,7 +801,7 @@ __global__ void __launch_bounds__((NW + 1) * 32,
                 }
                 const FastArgs& a = K.lv[lvl];
                 const int cx = tile_xs(a, txi + a.tx0) - HX;
-                const int cy = tile_ys(a, tyi + a.ty0) - H - 1;
+                const int cy = tile_ys(a, tyi + a.ty0) - H - KR;
                 if (i >= NS) wait_empty(s, (use - 1) & 1);
                 report(i - kRing + 1, true);  // ring slot i % kRing is free
                 row_ring[i & (kRing - 1)] = lvl == 0 ? b * f.R0 + tyi : -1;
@@ -777,7 +833,7 @@ __global__ void __launch_bounds__((NW + 1) * 32,
                         const int fb = t / a.ntiles_img, ft = t - fb * a.ntiles_img;
                         const int fy = ft / a.tiles_x;
                         const int fx0 = tile_xs(a, ft - fy * a.tiles_x + a.tx0) - HX;
-                        const int fy0 = tile_ys(a, fy + a.ty0) - H - 1;
+                        const int fy0 = tile_ys(a, fy + a.ty0) - H - KR;
                         const bool bd = fx0 < 0 || fy0 < 0 || fx0 + TWC > a.qw || fy0 + G::kRows > a.qh;
                         if (bd == (a.filter == 2)) break;
                     }
@@ -794,7 +850,7 @@ __global__ void __launch_bounds__((NW + 1) * 32,
                 const int tyi = a.xflag_a ? tile_row_of(tyk, a.ntiles_img / a.tiles_x, true) : tyk;
                 const int ty = tyi + a.ty0, tx = tt - tyk * a.tiles_x + a.tx0;
                 const int cx = tile_xs(a, tx) - HX;
-                const int cy = tile_ys(a, ty) - H - 1;
+                const int cy = tile_ys(a, ty) - H - KR;
                 if (a.xflag_a && !halo_ready && (cy < a.ylo || cy + G::kRows > a.yhi)) {
                     wait_halo_flags(a.xflag_a, a.xflag_b, a.xepoch, a.xerr);
                     halo_ready = true;
@@ -829,7 +885,7 @@ __global__ void __launch_bounds__((NW + 1) * 32,
                     const int fb = t / a.ntiles_img, ft = t - fb * a.ntiles_img;
                     const int fy = ft / a.tiles_x;
                     const int fx0 = tile_xs(a, ft - fy * a.tiles_x + a.tx0) - HX;
-                    const int fy0 = tile_ys(a, fy + a.ty0) - H - 1;
+                    const int fy0 = tile_ys(a, fy + a.ty0) - H - KR;
                     const bool bd = fx0 < 0 || fy0 < 0 || fx0 + TWC > a.qw || fy0 + G::kRows > a.qh;
                     if (bd != (a.filter == 2)) continue;
                 }
@@ -843,7 +899,7 @@ __global__ void __launch_bounds__((NW + 1) * 32,
                 const int tyi = a.xflag_a ? tile_row_of(tyk, a.ntiles_img / a.tiles_x, true) : tyk;
                 const int ty = tyi + a.ty0, tx = tt - tyk * a.tiles_x + a.tx0;
                 const int cx = tile_xs(a, tx) - HX;     // first compute cell column
-                const int cy = tile_ys(a, ty) - H - 1;  // ghost row above the region
+                const int cy = tile_ys(a, ty) - H - KR;  // ghost row above the region
                 if (a.xflag_a && !halo_ready && (cy < a.ylo || cy + G::kRows > a.yhi)) {
                     wait_halo_flags(a.xflag_a, a.xflag_b, a.xepoch, a.xerr);
                     halo_ready = true;
@@ -877,7 +933,7 @@ __global__ void __launch_bounds__((NW + 1) * 32,
     // release) one tile later, right before its next stores, when its
     // previous stores have long drained -- the fence then costs nothing.
     float v[R][CPT][4];
-    float gu[CPT][4], gd[CPT][4];
+    float gu[KR][CPT][4], gd[KR][CPT][4];  // KR ghost rows above / below
     int xslot = 0;
 
     for (int i = 0, t = blockIdx.x;; t += gridDim.x) {
@@ -911,7 +967,7 @@ __global__ void __launch_bounds__((NW + 1) * 32,
             const FastArgs& a = K.lv[decltype(L_)::value];
             const int ty = tyi + a.ty0, tx = txi + a.tx0;
             const int cx = tile_xs(a, tx) - HX;     // first compute cell column
-            const int cy = tile_ys(a, ty) - H - 1;  // ghost row above the region
+            const int cy = tile_ys(a, ty) - H - KR;  // ghost row above the region
             // Border tile: its compute region leaves the image. Periodic plans
             // load its cells with wrapped coordinates straight from global memory
             // (load-time wrap is exact for the periodic extension).
@@ -926,7 +982,7 @@ __global__ void __launch_bounds__((NW + 1) * 32,
             // TMA box and are never read as such -- before every neighbour step
             // the distance-1 ghosts are overwritten with their mirror images.
             const bool mtile = MIRROR && a.mirror && border;
-            const int gy0m = cy + 1 + warp * R;  // image row of v[0]
+            const int gy0m = cy + KR + warp * R;  // image row of v[0]
             if constexpr (!FUSED && !DIRECT)
                 if (!a.sched) mbar_wait(&full[s], phase);  // (dynamic: waited for the task)
 #ifdef WL_DIAG_TIMES
@@ -1038,10 +1094,12 @@ __global__ void __launch_bounds__((NW + 1) * 32,
                     }
                 }
             };
-            load_row(warp * R, gu);
 #pragma unroll
-            for (int r = 0; r < R; ++r) load_row(warp * R + 1 + r, v[r]);
-            load_row(warp * R + R + 1, gd);
+            for (int k = 0; k < KR; ++k) load_row(warp * R + k, gu[k]);
+#pragma unroll
+            for (int r = 0; r < R; ++r) load_row(warp * R + KR + r, v[r]);
+#pragma unroll
+            for (int k = 0; k < KR; ++k) load_row(warp * R + KR + R + k, gd[k]);
             // Release the stage: every lane's own loads are ordered before its
             // arrive (release semantics; a single elected arrive after __syncwarp
             // let the next TMA overwrite rows other lanes had not finished
@@ -1055,22 +1113,28 @@ __global__ void __launch_bounds__((NW + 1) * 32,
             if (DIR == 1 && a.scaling) {  // undo scaling first (transform.cpp:180)
 #pragma unroll
                 for (int c = 0; c < CPT; ++c) {
-                    gu[c][0] *= a.scale; gu[c][3] /= a.scale;
-                    gd[c][0] *= a.scale; gd[c][3] /= a.scale;
+#pragma unroll
+                    for (int k = 0; k < KR; ++k) {
+                        gu[k][c][0] *= a.scale; gu[k][c][3] /= a.scale;
+                        gd[k][c][0] *= a.scale; gd[k][c][3] /= a.scale;
+                    }
 #pragma unroll
                     for (int r = 0; r < R; ++r) { v[r][c][0] *= a.scale; v[r][c][3] /= a.scale; }
                 }
             }
 #pragma unroll
             for (int c = 0; c < CPT; ++c) {
-                P::pre(gu[c]);
-                P::pre(gd[c]);
+#pragma unroll
+                for (int k = 0; k < KR; ++k) {
+                    P::pre(gu[k][c]);
+                    P::pre(gd[k][c]);
+                }
 #pragma unroll
                 for (int r = 0; r < R; ++r) P::pre(v[r][c]);
             }
 
             // pair mode: the state as packed pairs A = (c0, c2), B = (c1, c3)
-            constexpr bool PM = PairMode<P>::on && CPT == 4 && !MIRROR && !FUSED;
+            constexpr bool PM = PairMode<P>::on && CPT == 4 && !MIRROR && !FUSED && KR == 1;
             wl2 v2[PM ? R : 1][2][4], gu2[2][4], gd2[2][4];
             if constexpr (PM) {
                 auto pack = [&](const float (&src)[CPT][4], wl2 (&dst)[2][4]) {
@@ -1080,8 +1144,8 @@ __global__ void __launch_bounds__((NW + 1) * 32,
                         dst[1][k] = wl_pk_keep(src[1][k], src[3][k]);
                     }
                 };
-                pack(gu, gu2);
-                pack(gd, gd2);
+                pack(gu[0], gu2);
+                pack(gd[KR - 1], gd2);
 #pragma unroll
                 for (int r = 0; r < R; ++r) pack(v[r], v2[r < (PM ? R : 1) ? r : 0]);
             }
@@ -1089,7 +1153,7 @@ __global__ void __launch_bounds__((NW + 1) * 32,
 #ifndef WL_DIAG_NO_COMPUTE
             sfor<P::kEpochs>([&](auto e_) {
                 constexpr int E = decltype(e_)::value;
-                constexpr unsigned long long U = P::kUse[E];
+                using UO = UseOf<P, E>;  // this epoch's neighbour reads (UO{} at the queries)
                 // Split-phase block barrier for epochs > 0: publish the edge rows
                 // and ARRIVE, compute the rows that need no neighbour-warp data,
                 // then WAIT and finish the two edge rows. Still exactly one
@@ -1100,7 +1164,7 @@ __global__ void __launch_bounds__((NW + 1) * 32,
                 // the components the warp below reads from its row above (UP), then
                 // its top row for those the warp above reads from below (DN). Each
                 // row is [lane] x CPT floats: one contiguous warp-wide access.
-                constexpr int NUP = xch_count(U, -1, XF), NDN = xch_count(U, 1, XF);
+                constexpr int NUP = xch_count(UO{}, -1, XF), NDN = xch_count(UO{}, 1, XF);
                 constexpr int kCompF = 32 * CPT;
                 constexpr int kSlotF = NXC * kCompF;
                 float* xw = xch + (xslot * NW + warp) * kSlotF;
@@ -1127,27 +1191,27 @@ __global__ void __launch_bounds__((NW + 1) * 32,
                     if constexpr (E > 0) {
                         sfor<4>([&](auto c_) {
                             constexpr int C = decltype(c_)::value;
-                            if constexpr (xch_up(U, C, XF))
-                                reinterpret_cast<ulonglong2*>(xw + xch_rank(U, C, -1, XF) * kCompF)[lane] =
+                            if constexpr (xch_up(UO{}, C, XF))
+                                reinterpret_cast<ulonglong2*>(xw + xch_rank(UO{}, C, -1, XF) * kCompF)[lane] =
                                     make_ulonglong2(v2[R - 1][0][C], v2[R - 1][1][C]);
-                            if constexpr (xch_dn(U, C, XF))
-                                reinterpret_cast<ulonglong2*>(xw + (NUP + xch_rank(U, C, 1, XF)) * kCompF)[lane] =
+                            if constexpr (xch_dn(UO{}, C, XF))
+                                reinterpret_cast<ulonglong2*>(xw + (NUP + xch_rank(UO{}, C, 1, XF)) * kCompF)[lane] =
                                     make_ulonglong2(v2[0][0][C], v2[0][1][C]);
                         });
                         named_sync(1, NW * 32);  // the epoch's block barrier
                         sfor<4>([&](auto c_) {
                             constexpr int C = decltype(c_)::value;
-                            if constexpr (xch_up(U, C, XF))
+                            if constexpr (xch_up(UO{}, C, XF))
                                 if (warp > 0) {
                                     const ulonglong2 q = reinterpret_cast<const ulonglong2*>(
-                                        xw - kSlotF + xch_rank(U, C, -1, XF) * kCompF)[lane];
+                                        xw - kSlotF + xch_rank(UO{}, C, -1, XF) * kCompF)[lane];
                                     gu2[0][C] = q.x;
                                     gu2[1][C] = q.y;
                                 }
-                            if constexpr (xch_dn(U, C, XF))
+                            if constexpr (xch_dn(UO{}, C, XF))
                                 if (warp < NW - 1) {
                                     const ulonglong2 q = reinterpret_cast<const ulonglong2*>(
-                                        xw + kSlotF + (NUP + xch_rank(U, C, 1, XF)) * kCompF)[lane];
+                                        xw + kSlotF + (NUP + xch_rank(UO{}, C, 1, XF)) * kCompF)[lane];
                                     gd2[0][C] = q.x;
                                     gd2[1][C] = q.y;
                                 }
@@ -1162,10 +1226,10 @@ __global__ void __launch_bounds__((NW + 1) * 32,
                             T < 0 ? gu2 : (T >= R ? gd2 : v2[T < 0 ? 0 : (T >= R ? R - 1 : T)]);
                         sfor<4>([&](auto c_) {
                             constexpr int C = decltype(c_)::value;
-                            constexpr bool nl = T < 0 ? uses(U, C, -1, -1)
-                                                      : (T >= R ? uses(U, C, 1, -1) : uses_dc(U, C, -1));
-                            constexpr bool nr = T < 0 ? uses(U, C, -1, 1)
-                                                      : (T >= R ? uses(U, C, 1, 1) : uses_dc(U, C, 1));
+                            constexpr bool nl = T < 0 ? uses(UO{}, C, -1, -1)
+                                                      : (T >= R ? uses(UO{}, C, 1, -1) : uses_dc(UO{}, C, -1));
+                            constexpr bool nr = T < 0 ? uses(UO{}, C, -1, 1)
+                                                      : (T >= R ? uses(UO{}, C, 1, 1) : uses_dc(UO{}, C, 1));
                             if constexpr (nl) {
                                 const float c3 = __shfl_up_sync(0xffffffffu, wl_hi(rw[1][C]), 1);
                                 lt[T + 1][C] = wl_pk_keep(c3, wl_lo(rw[1][C]));
@@ -1205,10 +1269,13 @@ __global__ void __launch_bounds__((NW + 1) * 32,
                 if constexpr (E > 0) {
                     sfor<4>([&](auto c_) {
                         constexpr int C = decltype(c_)::value;
-                        if constexpr (xch_up(U, C, XF))
-                            put(xw + xch_rank(U, C, -1, XF) * kCompF, v[R - 1], C);
-                        if constexpr (xch_dn(U, C, XF))
-                            put(xw + (NUP + xch_rank(U, C, 1, XF)) * kCompF, v[0], C);
+                        // rows R-1..R-n for the warp below, 0..n-1 for the warp above
+#pragma unroll
+                        for (int k = 0; k < xch_up(UO{}, C, XF); ++k)
+                            put(xw + (xch_rank(UO{}, C, -1, XF) + k) * kCompF, v[R - 1 - k], C);
+#pragma unroll
+                        for (int k = 0; k < xch_dn(UO{}, C, XF); ++k)
+                            put(xw + (NUP + xch_rank(UO{}, C, 1, XF) + k) * kCompF, v[k], C);
                     });
 #ifdef WL_BREAK_BARRIER
                     // negative control (acceptance.cpp:283-296 / parsim break_barrier):
@@ -1234,12 +1301,12 @@ __global__ void __launch_bounds__((NW + 1) * 32,
                         constexpr int T = decltype(k_)::value - 1;
                         constexpr bool edge = T < 0 || T >= R;
                         if constexpr (edge == decltype(gdgu)::value) {
-                            float (&dst)[CPT][4] = T < 0 ? gu : (T >= R ? gd : v[T < 0 ? 0 : (T >= R ? R - 1 : T)]);
+                            float (&dst)[CPT][4] = T < 0 ? gu[0] : (T >= R ? gd[0] : v[T < 0 ? 0 : (T >= R ? R - 1 : T)]);
                             if constexpr (T + 2 <= R - 1) {
                                 if (T == t_top)
                                     sfor<4>([&](auto c_) {
                                         constexpr int C = decltype(c_)::value;
-                                        if constexpr (uses_dr(U, C, -1))
+                                        if constexpr (uses_dr(UO{}, C, -1))
 #pragma unroll
                                             for (int c = 0; c < CPT; ++c) dst[c][C] = v[T + 2][c][C];
                                     });
@@ -1248,7 +1315,7 @@ __global__ void __launch_bounds__((NW + 1) * 32,
                                 if (T == t_bot)
                                     sfor<4>([&](auto c_) {
                                         constexpr int C = decltype(c_)::value;
-                                        if constexpr (uses_dr(U, C, 1))
+                                        if constexpr (uses_dr(UO{}, C, 1))
 #pragma unroll
                                             for (int c = 0; c < CPT; ++c) dst[c][C] = v[T - 2][c][C];
                                     });
@@ -1260,7 +1327,8 @@ __global__ void __launch_bounds__((NW + 1) * 32,
                 // neighbour as its own column 1; the lane whose last cell is column
                 // qw-1 reads its right neighbour as its own column qw-2 (cx and qw
                 // are multiples of CPT).
-                auto hfix = [&](float (&sl_)[R + 2][4], float (&sr_)[R + 2][4], int r_lo, int r_hi) {
+                auto hfix = [&](float (&sl_)[R + 2 * KR][KR][4], float (&sr_)[R + 2 * KR][KR][4], int r_lo,
+                                int r_hi) {
                     if (!mtile) return;
                     const int gxl = cx + CPT * lane;
                     const bool left = gxl == 0, right = gxl + CPT - 1 == a.qw - 1;
@@ -1268,31 +1336,31 @@ __global__ void __launch_bounds__((NW + 1) * 32,
                     for (int r = 0; r < R + 2; ++r) {
                         if (r < r_lo || r > r_hi) continue;
                         const float (&src)[CPT][4] =
-                            r == 0 ? gu : (r == R + 1 ? gd : v[r == 0 ? 0 : (r > R ? R - 1 : r - 1)]);
+                            r == 0 ? gu[0] : (r == R + 1 ? gd[0] : v[r == 0 ? 0 : (r > R ? R - 1 : r - 1)]);
                         sfor<4>([&](auto c_) {
                             constexpr int C = decltype(c_)::value;
-                            if constexpr (uses_dc(U, C, -1))
-                                if (left) sl_[r][C] = src[1][C];
-                            if constexpr (uses_dc(U, C, 1))
-                                if (right) sr_[r][C] = src[CPT - 2][C];
+                            if constexpr (uses_dc(UO{}, C, -1))
+                                if (left) sl_[r][0][C] = src[1][C];
+                            if constexpr (uses_dc(UO{}, C, 1))
+                                if (right) sr_[r][0][C] = src[CPT - 2][C];
                         });
                     }
                 };
                 if constexpr (MIRROR) vfix(std::false_type{});
                 // Horizontal neighbours of the lane's edge columns (warp shuffle).
-                float sl[R + 2][4], sr[R + 2][4];
+                float sl[R + 2 * KR][KR][4], sr[R + 2 * KR][KR][4];
                 sfor<4>([&](auto c_) {
                     constexpr int C = decltype(c_)::value;
-                    if constexpr (uses_dc(U, C, -1)) {
-#pragma unroll
-                        for (int r = 0; r < R; ++r)
-                            sl[r + 1][C] = __shfl_up_sync(0xffffffffu, v[r][CPT - 1][C], 1);
-                    }
-                    if constexpr (uses_dc(U, C, 1)) {
-#pragma unroll
-                        for (int r = 0; r < R; ++r)
-                            sr[r + 1][C] = __shfl_down_sync(0xffffffffu, v[r][0][C], 1);
-                    }
+                    sfor<KR>([&](auto j_) {
+                        constexpr int J = decltype(j_)::value;  // column -1-J / CPT+J
+                        sfor<R>([&](auto r_) {
+                            constexpr int r = decltype(r_)::value;
+                            if constexpr (reads(UO{}, C, r, -1 - J, R, CPT))
+                                sl[r + KR][J][C] = __shfl_up_sync(0xffffffffu, v[r][CPT - 1 - J][C], 1);
+                            if constexpr (reads(UO{}, C, r, CPT + J, R, CPT))
+                                sr[r + KR][J][C] = __shfl_down_sync(0xffffffffu, v[r][J][C], 1);
+                        });
+                    });
                 });
                 if constexpr (MIRROR) hfix(sl, sr, 1, R);
                 float o[R][CPT][4];
@@ -1300,39 +1368,53 @@ __global__ void __launch_bounds__((NW + 1) * 32,
                     constexpr int RR = decltype(r_)::value;
                     sfor<CPT>([&](auto c_) {
                         constexpr int CC = decltype(c_)::value;
-                        Acc<R, CPT, RR, CC> acc{v, gu, gd, sl, sr};
+                        Acc<R, CPT, KR, RR, CC> acc{v, gu, gd, sl, sr};
                         P::template nbr<E>(acc, o[RR][CC]);
                     });
                 };
-                // interior rows 1..R-2 read only this warp's rows
-                sfor<R - 2>([&](auto r_) { row(std::integral_constant<int, decltype(r_)::value + 1>{}); });
+                // interior rows KR..R-1-KR read only this warp's rows
+                sfor<R - 2 * KR>([&](auto r_) { row(std::integral_constant<int, decltype(r_)::value + KR>{}); });
                 if constexpr (E > 0) {
                     sfor<4>([&](auto c_) {
                         constexpr int C = decltype(c_)::value;
-                        if constexpr (xch_up(U, C, XF))  // bottom row of the warp above
-                            if (warp > 0) get(xw - kSlotF + xch_rank(U, C, -1, XF) * kCompF, gu, C);
-                        if constexpr (xch_dn(U, C, XF))  // top row of the warp below
+                        // bottom rows of the warp above -> gu[KR-1-k], top rows of the
+                        // warp below -> gd[k]
+#pragma unroll
+                        for (int k = 0; k < xch_up(UO{}, C, XF); ++k)
+                            if (warp > 0)
+                                get(xw - kSlotF + (xch_rank(UO{}, C, -1, XF) + k) * kCompF, gu[KR - 1 - k], C);
+#pragma unroll
+                        for (int k = 0; k < xch_dn(UO{}, C, XF); ++k)
                             if (warp < NW - 1)
-                                get(xw + kSlotF + (NUP + xch_rank(U, C, 1, XF)) * kCompF, gd, C);
+                                get(xw + kSlotF + (NUP + xch_rank(UO{}, C, 1, XF) + k) * kCompF, gd[k], C);
                     });
                     (void)NDN;
                     xslot ^= 1;
                 }
                 if constexpr (MIRROR) vfix(std::true_type{});
+                // lane-neighbour cells of the ghost rows (corners of the stencil)
                 sfor<4>([&](auto c_) {
                     constexpr int C = decltype(c_)::value;
-                    if constexpr (uses(U, C, -1, -1))
-                        sl[0][C] = __shfl_up_sync(0xffffffffu, gu[CPT - 1][C], 1);
-                    if constexpr (uses(U, C, 1, -1))
-                        sl[R + 1][C] = __shfl_up_sync(0xffffffffu, gd[CPT - 1][C], 1);
-                    if constexpr (uses(U, C, -1, 1))
-                        sr[0][C] = __shfl_down_sync(0xffffffffu, gu[0][C], 1);
-                    if constexpr (uses(U, C, 1, 1))
-                        sr[R + 1][C] = __shfl_down_sync(0xffffffffu, gd[0][C], 1);
+                    sfor<KR>([&](auto j_) {
+                        constexpr int J = decltype(j_)::value;
+                        sfor<KR>([&](auto k_) {
+                            constexpr int k = decltype(k_)::value;
+                            if constexpr (reads(UO{}, C, k - KR, -1 - J, R, CPT))
+                                sl[k][J][C] = __shfl_up_sync(0xffffffffu, gu[k][CPT - 1 - J][C], 1);
+                            if constexpr (reads(UO{}, C, R + k, -1 - J, R, CPT))
+                                sl[R + KR + k][J][C] = __shfl_up_sync(0xffffffffu, gd[k][CPT - 1 - J][C], 1);
+                            if constexpr (reads(UO{}, C, k - KR, CPT + J, R, CPT))
+                                sr[k][J][C] = __shfl_down_sync(0xffffffffu, gu[k][J][C], 1);
+                            if constexpr (reads(UO{}, C, R + k, CPT + J, R, CPT))
+                                sr[R + KR + k][J][C] = __shfl_down_sync(0xffffffffu, gd[k][J][C], 1);
+                        });
+                    });
                 });
                 if constexpr (MIRROR) hfix(sl, sr, 0, R + 1);  // corners (and rows again)
-                row(std::integral_constant<int, 0>{});
-                row(std::integral_constant<int, R - 1>{});
+                sfor<KR>([&](auto k_) {
+                    row(std::integral_constant<int, decltype(k_)::value>{});
+                    row(std::integral_constant<int, R - KR + decltype(k_)::value>{});
+                });
 #pragma unroll
                 for (int r = 0; r < R; ++r)
 #pragma unroll
@@ -1356,7 +1438,7 @@ __global__ void __launch_bounds__((NW + 1) * 32,
             }
 #endif  // WL_DIAG_NO_COMPUTE
             // ---------------- store ----------------
-            const int gy0 = cy + 1 + warp * R;  // global cell row of v[0]
+            const int gy0 = cy + KR + warp * R;  // global cell row of v[0]
             const int gx = cx + CPT * lane;     // global cell col of column 0
             if (DIR == 0 && a.scaling) {  // scale_planes (transform.cpp:154-159)
 #pragma unroll
@@ -1591,27 +1673,49 @@ struct Config;
 #endif
 template <>
 struct Config<0, 0> {  // cdf53 forward, halo 1
+    static constexpr int KR = 1;
     static constexpr int R = WL_R53F, NW = WL_NW53F, CPT = WL_CPT_FWD, NS = WL_NS53F;
     static constexpr bool XF = WL_XF53F;
     static constexpr int MAXB = 0;
 };
 template <>
 struct Config<0, 1> {  // cdf53 inverse
+    static constexpr int KR = 1;
     static constexpr int R = WL_R53I, NW = WL_NW53I, CPT = WL_CPT_INV, NS = WL_NS53I;
     static constexpr bool XF = WL_XF53I;
     static constexpr int MAXB = WL_MAXB53I;
 };
 template <>
 struct Config<1, 0> {  // cdf97 forward, halo 2
+    static constexpr int KR = 1;
     static constexpr int R = WL_R97F, NW = WL_NW97F, CPT = WL_CPT_FWD, NS = WL_NS97F;
     static constexpr bool XF = WL_XF97F;
     static constexpr int MAXB = 0;
 };
 template <>
 struct Config<1, 1> {  // cdf97 inverse
+    static constexpr int KR = 1;
     static constexpr int R = WL_R97I, NW = WL_NW97I, CPT = WL_CPT_INV, NS = WL_NS97I;
     static constexpr bool XF = WL_XF97I;
     static constexpr int MAXB = WL_MAXB97I;
+};
+
+// dd137 (reach 2: two ghost rows / lane-neighbour cells per side, halo 3),
+// lifting schemes only (Polyphase(*) stays on the interpreter): CPT = 4 both
+// directions, 32-row tiles (4 x 8 warps; the two-row edge exchange of 8
+// warps and the 36-row stage pair fit one CTA per SM).
+#ifndef WL_R137
+#define WL_R137 4
+#endif
+#ifndef WL_NW137
+#define WL_NW137 8
+#endif
+template <int DIR>
+struct Config<2, DIR> {
+    static constexpr int R = WL_R137, NW = WL_NW137, CPT = 4, NS = 2;
+    static constexpr bool XF = false;
+    static constexpr int MAXB = 0;
+    static constexpr int KR = 2;
 };
 
 // Per-scheme override of the geometry (scheme = SchemeKind index). The cdf97
@@ -1638,6 +1742,7 @@ struct SchemeConfig : Config<WAVELET, DIR> {};
 #endif
 template <int SCHEME>
 struct PolyInv {
+    static constexpr int KR = 1;
     static constexpr int R = WL_POLY_R, NW = WL_POLY_NW, CPT = 4, NS = WL_POLY_NS_INV;
     static constexpr bool XF = false;
     static constexpr int MAXB = 0;
@@ -1701,7 +1806,7 @@ struct Plan {
 //    last ones past its end) cost 7-10% redundant work at 8192^2 and its
 //    nearly-all-wrapped edge tiles made the launch's tail.
 inline Plan plan_tiles(const WlLevel& L, int H, int R, int NW, int CPT, bool no_mirror = false,
-                       bool legacy = false) {
+                       bool legacy = false, int KR = 1) {
     Plan p{};
     p.args.xlast = p.args.ylast = 0x7fffffff;
     const int nb = L.nb > 1 ? L.nb : 1;
@@ -1730,7 +1835,7 @@ inline Plan plan_tiles(const WlLevel& L, int H, int R, int NW, int CPT, bool no_
     // [ylo, yhi).
     const bool sym_window = L.boundary == 1 && L.yhi > 0;
     bool full_sym = L.boundary == 1 && L.qw >= 2 && L.qh >= 2 &&
-                    L.qw % CPT == 0 && WL_SYM_FAST && !no_mirror;
+                    L.qw % CPT == 0 && WL_SYM_FAST && !no_mirror && KR == 1;
     // Row offset of the symmetric grid: every tile whose compute rows hold
     // image row 0 must not have it as a warp's last row (its mirror source,
     // row 1, would sit in the next warp), nor row qh-1 as a warp's first row.
@@ -1751,14 +1856,14 @@ inline Plan plan_tiles(const WlLevel& L, int H, int R, int NW, int CPT, bool no_
     }
     const bool whole = L.boundary == 0 || (L.yhi > 0 && !sym_window) || full_sym;
     int X0 = wide ? (whole ? 0 : HX) : H;
-    const int Y0 = full_sym ? ysym : H + 1;
+    const int Y0 = full_sym ? ysym : H + KR;
     const int tx0 = wide ? 0 : -1;  // periodic plans
     int tx, ty;
     int y0 = Y0;
     p.args.mirror = full_sym ? 1 : 0;
     if (sym_window && (L.ylo < 0 || L.yhi > L.qh || L.yhi <= L.ylo)) return p;  // ok = false
     if (L.yhi > 0 && !sym_window) {
-        if (L.boundary != 0 || L.ylo < H + 1 || L.yhi > L.qh - H - 1 || L.yhi <= L.ylo)
+        if (L.boundary != 0 || L.ylo < H + KR || L.yhi > L.qh - H - KR || L.yhi <= L.ylo)
             return p;  // ok = false
         tx = (L.qw - X0 > 0 ? (L.qw - X0 + TW - 1) / TW : 0) - tx0;
         ty = (L.yhi - L.ylo + TH - 1) / TH;
@@ -1777,8 +1882,8 @@ inline Plan plan_tiles(const WlLevel& L, int H, int R, int NW, int CPT, bool no_
     } else {
         const int c0 = X0 - HX;  // first compute column of tile 0 (>= 0)
         tx = L.qw - c0 >= TWC ? (L.qw - c0 - TWC) / TW + 1 : 0;
-        const int span = L.qh - (Y0 - H - 1);  // rows available from the first ghost row
-        ty = span >= NW * R + 2 ? (span - (NW * R + 2)) / TH + 1 : 0;
+        const int span = L.qh - (Y0 - H - KR);  // rows available from the first ghost row
+        ty = span >= NW * R + 2 * KR ? (span - (NW * R + 2 * KR)) / TH + 1 : 0;
         p.args.tx0 = p.args.ty0 = 0;
         p.args.wrap = 0;
     }
@@ -1821,7 +1926,7 @@ inline Plan plan_tiles(const WlLevel& L, int H, int R, int NW, int CPT, bool no_
 // launch_fused).
 template <class P, int DIR, int R, int NW, int CPT, int NS, bool XF>
 bool level_args(const WlLevel& L, const Plan& plan, FastArgs& a, CUtensorMap (&maps)[4]) {
-    using G = Geometry<R, NW, CPT, NS, xch_comps<P, XF>()>;
+    using G = Geometry<R, NW, CPT, NS, xch_comps<P, XF>(), P::kReach>;
     constexpr int TWC = G::TWC;
     a = plan.args;
     const int nb = L.nb > 1 ? L.nb : 1;
@@ -1858,9 +1963,9 @@ bool level_args(const WlLevel& L, const Plan& plan, FastArgs& a, CUtensorMap (&m
 }
 
 // Persistent grid size of a kernel variant: SMs x resident CTAs (cached per device).
-template <int R, int NW, int CPT, int NS, int NXC, int MAXB, class Kern>
+template <int R, int NW, int CPT, int NS, int NXC, int MAXB, int KR, class Kern>
 int grid_cap(Kern kern, int* cache) {
-    using G = Geometry<R, NW, CPT, NS, NXC>;
+    using G = Geometry<R, NW, CPT, NS, NXC, KR>;
     int dev = 0;
     cudaGetDevice(&dev);
     int& mb = cache[dev & 63];
@@ -1881,14 +1986,14 @@ int grid_cap(Kern kern, int* cache) {
 template <class P, int DIR, int R, int NW, int CPT, int NS, bool XF, int MAXB>
 cudaError_t launch(const WlLevel& L, const Plan& plan, cudaStream_t stream) {
     constexpr int NXC = xch_comps<P, XF>();
-    using G = Geometry<R, NW, CPT, NS, NXC>;
+    using G = Geometry<R, NW, CPT, NS, NXC, P::kReach>;
     CUtensorMap maps[4];
     KArgs k{};
     if (!level_args<P, DIR, R, NW, CPT, NS, XF>(L, plan, k.lv[0], maps))
         return cudaErrorInvalidValue;
     static int cap_norm[64] = {}, cap_mirr[64] = {};
     auto run = [&](auto kern, int* cache, int filter) -> cudaError_t {
-        const int mb = grid_cap<R, NW, CPT, NS, NXC, MAXB>(kern, cache);
+        const int mb = grid_cap<R, NW, CPT, NS, NXC, MAXB, P::kReach>(kern, cache);
         KArgs f = k;
         f.lv[0].filter = filter;
         f.lv[0].sched = f.lv[0].ntiles > mb ? sched_slot(stream) : nullptr;
@@ -1898,12 +2003,18 @@ cudaError_t launch(const WlLevel& L, const Plan& plan, cudaStream_t stream) {
         wl_count_launch();
         return le != cudaSuccess ? le : cudaGetLastError();
     };
-    if (!k.lv[0].mirror) return run(fast_kernel<P, DIR, R, NW, CPT, NS, XF, false>, cap_norm, 0);
-    // symmetric whole-image plan: interior tiles on the plain kernel, the ring
-    // of border tiles on the mirroring variant (same grid, disjoint tiles)
-    cudaError_t e = run(fast_kernel<P, DIR, R, NW, CPT, NS, XF, false>, cap_norm, 1);
-    if (e != cudaSuccess) return e;
-    return run(fast_kernel<P, DIR, R, NW, CPT, NS, XF, true>, cap_mirr, 2);
+    if constexpr (P::kReach > 1) {  // no mirrored variant (plans never set mirror)
+        (void)cap_mirr;
+        if (k.lv[0].mirror) return cudaErrorNotSupported;
+        return run(fast_kernel<P, DIR, R, NW, CPT, NS, XF, false>, cap_norm, 0);
+    } else {
+        if (!k.lv[0].mirror) return run(fast_kernel<P, DIR, R, NW, CPT, NS, XF, false>, cap_norm, 0);
+        // symmetric whole-image plan: interior tiles on the plain kernel, the ring
+        // of border tiles on the mirroring variant (same grid, disjoint tiles)
+        cudaError_t e = run(fast_kernel<P, DIR, R, NW, CPT, NS, XF, false>, cap_norm, 1);
+        if (e != cudaSuccess) return e;
+        return run(fast_kernel<P, DIR, R, NW, CPT, NS, XF, true>, cap_mirr, 2);
+    }
 }
 
 // Direct-load launch (no TMA, element-wise stores): shapes the TMA path
@@ -1912,7 +2023,7 @@ cudaError_t launch(const WlLevel& L, const Plan& plan, cudaStream_t stream) {
 template <class P, int DIR, int R, int NW, int CPT, int NS, bool XF, int MAXB>
 cudaError_t launch_direct(const WlLevel& L, const Plan& plan, cudaStream_t stream) {
     constexpr int NXC = xch_comps<P, XF>();
-    using G = Geometry<R, NW, CPT, NS, NXC>;
+    using G = Geometry<R, NW, CPT, NS, NXC, P::kReach>;
     if (plan.args.mirror) return cudaErrorNotSupported;
     KArgs k{};
     FastArgs& a = k.lv[0];
@@ -1963,7 +2074,7 @@ cudaError_t launch_fused(const WlLevel& L0, const Plan& p0, const WlLevel& L1, c
         return cudaErrorNotSupported;
     } else {
         constexpr int NXC = xch_comps<P, XF>();
-        using G = Geometry<R, NW, CPT, NS, NXC>;
+        using G = Geometry<R, NW, CPT, NS, NXC, P::kReach>;
         CUtensorMap maps0[4], maps1[4];
         KArgs k{};
         if (!level_args<P, DIR, R, NW, CPT, NS, XF>(L0, p0, k.lv[0], maps0) ||
@@ -1987,7 +2098,7 @@ cudaError_t launch_fused(const WlLevel& L0, const Plan& p0, const WlLevel& L1, c
         f.target = (unsigned)f.X0n * NW;
         static int cap[64] = {};
         auto kern = fast_kernel<P, DIR, R, NW, CPT, NS, XF, false, true>;
-        const int mb = grid_cap<R, NW, CPT, NS, NXC, MAXB>(kern, cap);
+        const int mb = grid_cap<R, NW, CPT, NS, NXC, MAXB, P::kReach>(kern, cap);
         const int ntasks = f.n0 + f.n1;
         const int grid = ntasks < mb ? ntasks : mb;
         cudaError_t e = cudaMemsetAsync(ctr, 0, (2 + (size_t)nb * f.R0) * sizeof(unsigned), stream);

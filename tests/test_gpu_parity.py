@@ -208,13 +208,22 @@ def test_cross_scheme_agreement_large(wl):
         assert d <= 1e-5, (s, d)
 
 
-def test_dd137_interpreter(wl, oracle):
-    img = dyadic(40, 56, 3)
-    for s in ("sweldens", "monolithic_star", "polyphase", "convolution"):
-        for b in BOUNDARIES:
-            want = oracle.forward(img, "dd137", s, b)
-            got = host(wl.forward(gpu(img), wl.build_scheme(s, "dd137"), b))
-            assert rel_err(got, want) <= TOL, (s, b)
+@pytest.mark.parametrize("engine", [0, 1])
+def test_dd137_small(wl, oracle, engine):
+    """dd137 (reach 2, halo 3) on images smaller than one tile: the fast
+    engine's lifting kernels (engine 0; Polyphase on the interpreter) and the
+    interpreter alone (engine 1)."""
+    wl.set_engine(engine)
+    try:
+        for (h, w) in ((40, 56), (64, 200)):
+            img = dyadic(h, w, 3)
+            for s in ("sweldens", "iwahashi", "monolithic_star", "polyphase", "convolution"):
+                for b in BOUNDARIES:
+                    want = oracle.forward(img, "dd137", s, b)
+                    got = host(wl.forward(gpu(img), wl.build_scheme(s, "dd137"), b))
+                    assert rel_err(got, want) <= TOL, (s, b, h, w)
+    finally:
+        wl.set_engine(0)
 
 
 def test_errors(wl):

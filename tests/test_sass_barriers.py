@@ -29,7 +29,7 @@ def barrier_counts(lib_path):
         m = re.search(r"Function : (\S+)", line)
         if m:
             name = m.group(1)
-            km = re.search(r"fast_kernelI\d+P_(cdf\d+)_(\w+?)_(fwd|inv)", name)
+            km = re.search(r"fast_kernelI\d+P_(cdf\d+|dd137)_(\w+?)_(fwd|inv)", name)
             fn = km.groups() + (name,) if km else None
             if fn:
                 counts.setdefault(fn, 0)
@@ -43,10 +43,12 @@ def barrier_counts(lib_path):
 def test_sass_barriers_equal_count_barriers():
     counts = barrier_counts(wl.LIB_PATH)
     programs = {k[:3] for k in counts}
-    assert len(programs) == 2 * 9 * 2, sorted(programs)
-    # plain + mirroring + direct-load variant; forwards also the fused
-    # two-level variant
-    assert len(counts) == 3 * len(programs) + 2 * 9, len(counts)
+    # cdf53 / cdf97: 9 lifting schemes x 2 directions; dd137: 7 (Polyphase(*)
+    # stays on the interpreter)
+    assert len(programs) == 2 * 9 * 2 + 7 * 2, sorted(programs)
+    # cdf53 / cdf97: plain + mirroring + direct-load variant, forwards also the
+    # fused two-level variant; dd137 (reach 2): plain + direct-load
+    assert len(counts) == 3 * 36 + 18 + 2 * 14, len(counts)
     kinds = {"direct": 0, "fused": 0}
     for (w, s, d, name), n in counts.items():
         want = wl.build_scheme(s, w).info(0 if d == "fwd" else 1)["barriers"]
@@ -58,7 +60,7 @@ def test_sass_barriers_equal_count_barriers():
             kinds["fused"] += 1
         kinds["direct"] += direct
         assert n == want, (w, s, d, n, want)
-    assert kinds == {"direct": 36, "fused": 18}, kinds
+    assert kinds == {"direct": 36 + 14, "fused": 18}, kinds
 
 
 def variant_flags(name):

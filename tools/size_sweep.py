@@ -15,6 +15,8 @@ sys.path.insert(0, ROOT)
 import paper_1605_00561_b200 as wl  # noqa: E402
 
 sizes = [int(x) for x in sys.argv[1].split(",")]
+if os.environ.get("ENGINE"):  # 1 = generic interpreter, 3 = fast engine direct-load variant
+    wl.set_engine(int(os.environ["ENGINE"]))
 G = int(os.environ.get("G", "10"))
 ROUNDS = int(os.environ.get("ROUNDS", "7"))
 SLEEP = int(os.environ.get("SLEEP", "4000000"))  # cycles (~2 ms) of GPU sleep before each group
