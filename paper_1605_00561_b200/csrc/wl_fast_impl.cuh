@@ -1701,18 +1701,36 @@ struct Config<1, 1> {  // cdf97 inverse
 };
 
 // dd137 (reach 2: two ghost rows / lane-neighbour cells per side, halo 3),
-// lifting schemes only (Polyphase(*) stays on the interpreter): CPT = 4 both
-// directions, 32-row tiles (4 x 8 warps; the two-row edge exchange of 8
-// warps and the 36-row stage pair fit one CTA per SM).
+// lifting schemes only (Polyphase(*) stays on the interpreter). Forward:
+// CPT = 4, 32-row tiles (4 x 8 warps; the two-row edge exchange of 8 warps
+// and the 36-row stage pair fit one CTA per SM).
 #ifndef WL_R137
 #define WL_R137 4
 #endif
 #ifndef WL_NW137
 #define WL_NW137 8
 #endif
-template <int DIR>
-struct Config<2, DIR> {
+// inverse: CPT = 2, 6 x 6 (3-18% faster than the forwards' geometry,
+// profiles/tuning_r02_s2.txt)
+#ifndef WL_R137I
+#define WL_R137I 6
+#endif
+#ifndef WL_NW137I
+#define WL_NW137I 6
+#endif
+#ifndef WL_CPT137I
+#define WL_CPT137I 2
+#endif
+template <>
+struct Config<2, 0> {
     static constexpr int R = WL_R137, NW = WL_NW137, CPT = 4, NS = 2;
+    static constexpr bool XF = false;
+    static constexpr int MAXB = 0;
+    static constexpr int KR = 2;
+};
+template <>
+struct Config<2, 1> {
+    static constexpr int R = WL_R137I, NW = WL_NW137I, CPT = WL_CPT137I, NS = 2;
     static constexpr bool XF = false;
     static constexpr int MAXB = 0;
     static constexpr int KR = 2;
