@@ -9,6 +9,16 @@
 
 namespace wlfast {
 
+// Which (wavelet, direction) launches claim tiles dynamically: bit
+// 2 * wavelet + direction (cdf53 fwd 0x1, inv 0x2; cdf97 0x4 / 0x8; dd137
+// 0x10 / 0x20). Measured per direction (profiles/tuning_r02_s2.txt, bench on
+// one box): the cdf53 forwards and the cdf97 inverses need them at 16384^2
+// (0.40 -> 0.32 ms, 0.45 -> 0.33 ms); the one-CTA-per-SM cdf97 forwards are
+// 2-3% faster at 8192^2 and in the configs[3] pyramid with static tiles.
+#ifndef WL_DYN_DEFAULT_MASK
+#define WL_DYN_DEFAULT_MASK 0x3b
+#endif
+
 // Dynamic tile-claim counters (FastArgs::sched): one zeroed device ring per
 // device; a slot is {claim counter, exit counter} and the last CTA of the
 // launch using it resets it to zero. Eager launches cycle through the first
@@ -17,6 +27,14 @@ namespace wlfast {
 // their own from the rest, never reused (a replay may run concurrently with
 // eager launches); none left -> nullptr (static round robin). WL_DYN=0 turns
 // dynamic claims off.
+bool dyn_claims(int wavelet, int dir) {
+    static const int mask = [] {
+        const char* e = getenv("WL_DYN_MASK");
+        return e ? (int)strtol(e, nullptr, 0) : WL_DYN_DEFAULT_MASK;
+    }();
+    return (mask >> (2 * wavelet + dir)) & 1;
+}
+
 unsigned* sched_slot(cudaStream_t stream) {
     constexpr int kEager = 4096, kSlots = 8192;
     static std::mutex mu;

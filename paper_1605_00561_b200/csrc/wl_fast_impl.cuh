@@ -145,6 +145,19 @@ __device__ __forceinline__ void mbar_wait_backoff(uint64_t* b, unsigned parity) 
         ns = ns < CAP ? 2 * ns : CAP;
     }
 }
+#ifndef WL_CLAIM_LATE
+#define WL_CLAIM_LATE 0
+#endif
+// A/B knobs: border tiles of periodic plans from the TMA box + wrapped
+// re-reads of the outside cells (1) or every cell from global memory (0);
+// periodic grid from cell 0 with clamped last row/column (1) or the former
+// grid with a tile row/column before the image (0).
+#ifndef WL_BORDER_TMA
+#define WL_BORDER_TMA 1
+#endif
+#ifndef WL_PLAN_V2
+#define WL_PLAN_V2 1
+#endif
 // Fused pyramid launches: tasks claimed per atomic.
 #ifndef WL_FUSE_CLAIM
 #define WL_FUSE_CLAIM 4
@@ -823,11 +836,19 @@ __global__ void __launch_bounds__((NW + 1) * 32,
             // left 7-20 us between the first and the last CTA to finish at
             // 8192^2, tools/diag_times.py). The tile index goes to the compute
             // warps through task_sm; -1 ends their loop.
+            // WL_CLAIM_LATE: claim the next tile only once a stage is free (a CTA
+            // then holds at most NS tiles, not NS + 1, when the counter runs
+            // out -- a shorter tail), paying the atomic's round trip before the
+            // load instead of overlapping it.
             bool halo_ready = false;
             int t = blockIdx.x;
             for (int i = 0;; ++i) {
                 const int s = i % NS;
                 const unsigned use = i / NS;
+                if (WL_CLAIM_LATE) {
+                    if (i >= NS) mbar_wait_backoff<ProdBackoff<P, DIR>::ns>(&empty[s], (use - 1) & 1);
+                    if (i > 0) t = gridDim.x + (int)atomicAdd(a.sched, 1u);
+                }
                 if (a.filter) {  // interior-only / border-only launch of a symmetric plan
                     for (; t < a.ntiles; t = gridDim.x + (int)atomicAdd(a.sched, 1u)) {
                         const int fb = t / a.ntiles_img, ft = t - fb * a.ntiles_img;
@@ -838,7 +859,8 @@ __global__ void __launch_bounds__((NW + 1) * 32,
                         if (bd == (a.filter == 2)) break;
                     }
                 }
-                if (i >= NS) mbar_wait_backoff<ProdBackoff<P, DIR>::ns>(&empty[s], (use - 1) & 1);
+                if (!WL_CLAIM_LATE && i >= NS)
+                    mbar_wait_backoff<ProdBackoff<P, DIR>::ns>(&empty[s], (use - 1) & 1);
                 if (t >= a.ntiles) {
                     task_sm[s] = make_int4(-1, 0, 0, 0);
                     mbar_arrive(&full[s]);  // consumers see the sentinel and stop
@@ -870,7 +892,7 @@ __global__ void __launch_bounds__((NW + 1) * 32,
                     tma_load_3d(dst + 2 * plane, &m2, &full[s], cx, cy, b);
                     tma_load_3d(dst + 3 * plane, &m3, &full[s], cx, cy, b);
                 }
-                t = gridDim.x + (int)atomicAdd(a.sched, 1u);  // next claim overlaps the load
+                if (!WL_CLAIM_LATE) t = gridDim.x + (int)atomicAdd(a.sched, 1u);  // overlaps the load
             }
             // the last producer out resets the slot for the next launch using it
             // (every producer's final claim precedes its exit count)
@@ -1023,7 +1045,7 @@ __global__ void __launch_bounds__((NW + 1) * 32,
             // the 2x2 polyphase components.
             auto load_row = [&](int q, float (&dst)[CPT][4]) {
                 // q: cell row in the stage (0 = ghost row above the region)
-                if (DIRECT) {
+                if (DIRECT || (!WL_BORDER_TMA && wrap_tile)) {
                     const int ry = wrapi(cy + q, a.qh);
 #pragma unroll
                     for (int j = 0; j < CPT; ++j) load_cell(ry, wrapi(cx + CPT * lane + j, a.qw), dst[j]);
@@ -1079,7 +1101,7 @@ __global__ void __launch_bounds__((NW + 1) * 32,
                         }
                     }
                 }
-                if (wrap_tile) {
+                if (WL_BORDER_TMA && wrap_tile) {
                     // Border tile of a periodic plan: the TMA box is zero-filled
                     // outside the image; only those cells are re-read from their
                     // wrapped positions (exact for the periodic extension). The
@@ -1593,6 +1615,9 @@ using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t
 EncodeTiledFn encode_fn();
 // Claim-counter slot for a launch on `stream` (wl_fast.cu); nullptr = static.
 unsigned* sched_slot(cudaStream_t stream);
+// Dynamic claims for (wavelet, direction)? (wl_fast.cu: default table,
+// WL_DYN_MASK bit 2 * wavelet + direction overrides, WL_DYN=0 all off)
+bool dyn_claims(int wavelet, int dir);
 
 // 3-D map (w, h, nb images at `bstride` elements apart) of a float32 buffer;
 // box = box_w x box_h x 1.
@@ -1665,11 +1690,14 @@ struct Config;
 #ifndef WL_NW53I
 #define WL_NW53I 8
 #endif
+// cdf97 inverses: 5 x 8 (40-row tiles, 16 compute warps per SM) since the
+// dynamic tile claims; was 8 x 4 (profiles/tuning_r02_s2.txt: sweldens 8192^2
+// 0.101 -> 0.094 ms, 16384^2 0.384 -> 0.331 ms)
 #ifndef WL_R97I
-#define WL_R97I 8
+#define WL_R97I 5
 #endif
 #ifndef WL_NW97I
-#define WL_NW97I 4
+#define WL_NW97I 8
 #endif
 template <>
 struct Config<0, 0> {  // cdf53 forward, halo 1
@@ -1789,15 +1817,25 @@ struct SchemeConfig<WL_OVR_W, WL_OVR_D, WL_OVR_S> : Config<WL_OVR_W, WL_OVR_D> {
 };
 #endif
 
-// cdf97 Monolithic / Monolithic* inverses: full exchange measured faster
-// (profiles/tuning_r01_exchange.txt).
+// cdf97 Monolithic / Monolithic* inverses: the full exchange measured faster
+// at 8 x 4 (profiles/tuning_r01_exchange.txt); at 5 x 8 the minimal exchange
+// keeps two CTAs per SM and wins (0.103 / 0.096 ms vs 0.111 / 0.106 ms at
+// 8192^2, profiles/tuning_r02_s2.txt). Knobs for A/B builds.
+#ifndef WL_RMONO97I
+#define WL_RMONO97I WL_R97I
+#endif
+#ifndef WL_XFMONO97I
+#define WL_XFMONO97I WL_XF97I
+#endif
 template <>
 struct SchemeConfig<1, 1, 5> : Config<1, 1> {
-    static constexpr bool XF = true;
+    static constexpr bool XF = WL_XFMONO97I;
+    static constexpr int R = WL_RMONO97I;
 };
 template <>
 struct SchemeConfig<1, 1, 6> : Config<1, 1> {
-    static constexpr bool XF = true;
+    static constexpr bool XF = WL_XFMONO97I;
+    static constexpr int R = WL_RMONO97I;
 };
 
 struct Plan {
@@ -1905,7 +1943,7 @@ inline Plan plan_tiles(const WlLevel& L, int H, int R, int NW, int CPT, bool no_
         p.args.tx0 = p.args.ty0 = 0;
         p.args.wrap = 0;
     }
-    if (L.boundary == 0 && !legacy && (whole || (L.yhi > 0 && !sym_window))) {
+    if (WL_PLAN_V2 && L.boundary == 0 && !legacy && (whole || (L.yhi > 0 && !sym_window))) {
         // X0 - HX = -4: box starts stay 16-byte aligned (TW = 0 mod 4 when CPT = 2)
         const int Xp = wide ? 0 : H - 4;
         tx = L.qw - Xp > 0 ? (L.qw - Xp + TW - 1) / TW : 0;
@@ -2014,7 +2052,7 @@ cudaError_t launch(const WlLevel& L, const Plan& plan, cudaStream_t stream) {
         const int mb = grid_cap<R, NW, CPT, NS, NXC, MAXB, P::kReach>(kern, cache);
         KArgs f = k;
         f.lv[0].filter = filter;
-        f.lv[0].sched = f.lv[0].ntiles > mb ? sched_slot(stream) : nullptr;
+        f.lv[0].sched = f.lv[0].ntiles > mb && dyn_claims(L.wavelet, DIR) ? sched_slot(stream) : nullptr;
         const int grid = f.lv[0].ntiles < mb ? f.lv[0].ntiles : mb;
         cudaError_t le = launch_pdl(kern, dim3(grid), dim3((NW + 1) * 32), G::kSmemBytes,
                                     stream, maps[0], maps[1], maps[2], maps[3], f);
