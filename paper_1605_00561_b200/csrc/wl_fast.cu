@@ -211,12 +211,12 @@ bool tma_ok(const WlLevel& L, int CPT) {
     return true;
 }
 
-// The direct-load path: cp.async of pixel pairs (forward) / cells (inverse),
-// scalar stores; no halo wait (the strip runtime then waits in its
+// The direct-load path: float2 loads of pixel pairs (forward), scalar
+// everything else; no halo wait (the strip runtime then waits in its
 // exchange kernel).
 bool direct_ok(const WlLevel& L) {
     if (L.xflag_a) return false;
-    if (L.direction == 0) {  // 8-byte cp.async of pixel pairs
+    if (L.direction == 0) {  // float2 loads of pixel pairs: every row 8-byte aligned
         if (!aligned(L.in[0], 8) || L.in_pitch % 2 != 0) return false;
         if (L.nb > 1 && L.in_bstride[0] % 2 != 0) return false;
     }

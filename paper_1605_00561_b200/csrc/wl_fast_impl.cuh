@@ -603,12 +603,10 @@ constexpr int xch_comps() {
 
 // DIRECT: no TMA -- shapes whose pitches/pointers/widths the TMA boxes and
 // the aligned float4 stores cannot take (e.g. 8190^2 images: 32760-byte rows,
-// odd plane widths). The producer warp fills the same stage ring with
-// cp.async copies (8-byte pixel pairs forward, 4-byte cells inverse; wrapped
-// source coordinates, so border tiles need no fix-up) completing the stage's
-// mbarrier (cp.async.mbarrier.arrive.noinc, one arrival per producer lane);
-// the compute warps read it like a TMA stage and store element by element
-// under a column mask. Same instruction sequence per cell, same results.
+// odd plane widths). Every tile loads its cells with coalesced per-lane
+// global loads (the periodic border-tile path) and stores element by element
+// under a column mask; the producer warp exits at once and the stage ring is
+// not allocated. Same instruction sequence per cell, so the same results.
 template <class P, int DIR, int R, int NW, int CPT, int NS, bool XF, bool MIRROR,
           bool FUSED = false, bool DIRECT = false>
 __global__ void __launch_bounds__((NW + 1) * 32,
@@ -634,7 +632,7 @@ __global__ void __launch_bounds__((NW + 1) * 32,
     constexpr int HX = halo_x<CPT, H>();
     extern __shared__ __align__(128) unsigned char smem_raw[];
     float* stage = reinterpret_cast<float*>(smem_raw);
-    float* xch = stage + NS * G::kStageFloats;
+    float* xch = stage + (DIRECT ? 0 : NS * G::kStageFloats);
     uint64_t* full = reinterpret_cast<uint64_t*>(xch + G::kXchFloats);
     uint64_t* empty = full + NS;
 
@@ -652,7 +650,7 @@ __global__ void __launch_bounds__((NW + 1) * 32,
 #endif
     if (threadIdx.x == 0) {
         for (int k = 0; k < NS; ++k) {
-            mbar_init(&full[k], DIRECT ? 32 : 1);  // DIRECT: every producer lane's copies
+            mbar_init(&full[k], 1);
             mbar_init(&empty[k], NW * 32);
         }
         if (FUSED)
@@ -667,67 +665,7 @@ __global__ void __launch_bounds__((NW + 1) * 32,
 
     if (warp == NW) {
         // ---------------- producer warp: TMA tile stream ----------------
-        if constexpr (DIRECT) {
-            // periodic wrap: one conditional add/subtract unless the image is
-            // smaller than a tile (then the general modulo)
-            const bool small = a.qw < TWC || a.qh < G::kRows;
-            auto wrapd = [small](int i, int n) {
-                if (small) {
-                    i %= n;
-                    return i < 0 ? i + n : i;
-                }
-                return i < 0 ? i + n : (i >= n ? i - n : i);
-            };
-            for (int i = 0, t = blockIdx.x; t < a.ntiles; t += gridDim.x, ++i) {
-                const int s = i % NS;
-                const unsigned use = i / NS;
-                if (i >= NS) mbar_wait_backoff<ProdBackoff<P, DIR>::ns>(&empty[s], (use - 1) & 1);
-                const int b = t / a.ntiles_img, tt = t - b * a.ntiles_img;
-                const int tyk = tt / a.tiles_x;
-                const int ty = tyk + a.ty0, tx = tt - tyk * a.tiles_x + a.tx0;
-                const int cx = tile_xs(a, tx) - HX;
-                const int cy = tile_ys(a, ty) - H - KR;
-                const unsigned dst0 = smem_u32(stage + s * G::kStageFloats);
-                // this lane's wrapped cell columns (same for every row)
-                int rx[CPT];
-#pragma unroll
-                for (int k = 0; k < CPT; ++k) rx[k] = wrapd(cx + lane + 32 * k, a.qw);
-                if (DIR == 0) {
-                    const float* img = a.in[0] + b * a.in_bstride[0];
-                    for (int q = 0; q < G::kRows; ++q) {
-                        const float* r0 = img + (long)(2 * wrapd(cy + q, a.qh)) * a.in_pitch;
-#pragma unroll
-                        for (int r2 = 0; r2 < 2; ++r2)
-#pragma unroll
-                            for (int k = 0; k < CPT; ++k)
-                                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
-                                                 dst0 + 4u * ((2 * q + r2) * (2 * TWC) + 2 * (lane + 32 * k))),
-                                             "l"(r0 + r2 * a.in_pitch + 2 * rx[k])
-                                             : "memory");
-                    }
-                } else {
-#pragma unroll
-                    for (int c = 0; c < 4; ++c) {
-                        const float* pl = a.in[c] + b * a.in_bstride[c];
-                        for (int q = 0; q < G::kRows; ++q) {
-                            const float* r0 = pl + (long)wrapd(cy + q, a.qh) * a.in_pitch;
-#pragma unroll
-                            for (int k = 0; k < CPT; ++k)
-                                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
-                                                 dst0 + 4u * (c * TWC * G::kRows + q * TWC + lane + 32 * k)),
-                                             "l"(r0 + rx[k])
-                                             : "memory");
-                        }
-                    }
-                }
-                asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(
-                                 smem_u32(&full[s]))
-                             : "memory");
-            }
-            // the copies of the last tiles must land before the warp may exit
-            asm volatile("cp.async.wait_all;" ::: "memory");
-            return;
-        }
+        if constexpr (DIRECT) return;  // compute warps load their own cells
         if (FUSED && lane == 0) {
             const FuseArgs& f = K.fu;
             // Level-l tasks are claimed in chunks of kClaim, the next chunk one
@@ -1059,14 +997,15 @@ __global__ void __launch_bounds__((NW + 1) * 32,
             if (a.filter && border != (a.filter == 2)) return;  // the other launch's tile
             const unsigned phase = (i / NS) & 1;  // fill count of stage s (processed tiles)
             ++i;
-            // (DIRECT: the producer wrapped every source cell already)
-            const bool wrap_tile = !DIRECT && a.wrap && border;
+            // DIRECT: every tile loads from global memory (coordinates wrapped,
+            // which is the identity inside the image)
+            const bool wrap_tile = DIRECT || (a.wrap && border);
             // Symmetric border tile: out-of-image cells come zero-filled from the
             // TMA box and are never read as such -- before every neighbour step
             // the distance-1 ghosts are overwritten with their mirror images.
             const bool mtile = MIRROR && a.mirror && border;
             const int gy0m = cy + KR + warp * R;  // image row of v[0]
-            if constexpr (!FUSED)
+            if constexpr (!FUSED && !DIRECT)
                 if (!a.sched) mbar_wait(&full[s], phase);  // (dynamic: waited for the task)
 #ifdef WL_DIAG_TIMES
             if (dg && threadIdx.x == 0 && diag_tiles++ == 0) dg[1] = gtime();
@@ -1106,7 +1045,7 @@ __global__ void __launch_bounds__((NW + 1) * 32,
             // the 2x2 polyphase components.
             auto load_row = [&](int q, float (&dst)[CPT][4]) {
                 // q: cell row in the stage (0 = ghost row above the region)
-                if (!WL_BORDER_TMA && wrap_tile) {
+                if (DIRECT || (!WL_BORDER_TMA && wrap_tile)) {
                     const int ry = wrapi(cy + q, a.qh);
 #pragma unroll
                     for (int j = 0; j < CPT; ++j) load_cell(ry, wrapi(cx + CPT * lane + j, a.qw), dst[j]);
@@ -1188,8 +1127,10 @@ __global__ void __launch_bounds__((NW + 1) * 32,
             // let the next TMA overwrite rows other lanes had not finished
             // reading), and the proxy fence orders these generic-proxy reads
             // before the async-proxy (TMA) writes of the refill.
-            if constexpr (!DIRECT) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            mbar_arrive(&empty[s]);
+            if constexpr (!DIRECT) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                mbar_arrive(&empty[s]);
+            }
 
             if (DIR == 1 && a.scaling) {  // undo scaling first (transform.cpp:180)
 #pragma unroll
@@ -1865,6 +1806,28 @@ struct SchemeConfig<1, 0, 7> : Config<1, 0> {
     static constexpr int NW = WL_POLY_NW;
 };
 
+// cdf97 Iwahashi(*) / Explosive(*) forwards (three neighbour epochs): 40-row
+// tiles as 4 x 10 warps, 2-4% faster than 5 x 8 (profiles/tuning_r02_s2.txt,
+// variant f410); Sweldens and Monolithic(*) keep 5 x 8.
+#ifndef WL_R97F_IE
+#define WL_R97F_IE 4
+#endif
+#ifndef WL_NW97F_IE
+#define WL_NW97F_IE 10
+#endif
+template <int SCHEME>
+struct Fwd97IE : Config<1, 0> {
+    static constexpr int R = WL_R97F_IE, NW = WL_NW97F_IE;
+};
+template <>
+struct SchemeConfig<1, 0, 1> : Fwd97IE<1> {};
+template <>
+struct SchemeConfig<1, 0, 2> : Fwd97IE<2> {};
+template <>
+struct SchemeConfig<1, 0, 3> : Fwd97IE<3> {};
+template <>
+struct SchemeConfig<1, 0, 4> : Fwd97IE<4> {};
+
 // Tuning knob: one extra per-scheme override from the compiler command line
 // (-DWL_OVR_W=w -DWL_OVR_D=d -DWL_OVR_S=s -DWL_OVR_R=.. -DWL_OVR_NW=.. -DWL_OVR_NS=..
 // -DWL_OVR_XF=..), for A/B builds.
@@ -2158,7 +2121,7 @@ cudaError_t launch_direct(const WlLevel& L, const Plan& plan, cudaStream_t strea
     a.scaling = L.scaling && wl_host_program(L.prog).has_scale;
     a.scale = wl_host_program(L.prog).scale;
     a.filter = 0;
-    constexpr size_t smem = G::kSmemBytes;  // the stage ring filled by cp.async
+    constexpr size_t smem = (size_t)G::kXchFloats * 4 + 16 * NS;
     auto kern = fast_kernel<P, DIR, R, NW, CPT, NS, XF, false, false, true>;
     static int cap[64] = {};
     int dev = 0;
