@@ -14,7 +14,8 @@ sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 from summarize_profiles import PROGRAMS, read_metrics_csv, short, to_bytes, to_us  # noqa: E402
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-GO = os.path.join(ROOT, "gpurun_out", "r02")
+TAG = sys.argv[1] if len(sys.argv) > 1 else "r02"
+GO = os.path.join(ROOT, "gpurun_out", TAG)
 PR = os.path.join(ROOT, "profiles")
 C3 = ["cdf97/monolithic_star", "cdf97/monolithic", "cdf97/sweldens", "cdf53/monolithic",
       "cdf53/monolithic_star"]
@@ -36,32 +37,32 @@ def traffic(path, progs, n, prefix=""):
 
 
 def main():
-    t = traffic(os.path.join(GO, "traffic_r02.csv"), PROGRAMS, 8192)
-    t.update(traffic(os.path.join(GO, "traffic_c3_r02.csv"), C3, 16384, "c3/"))
-    json.dump({k: v["total"] for k, v in t.items()}, open(os.path.join(PR, "traffic_r02.json"), "w"),
+    t = traffic(os.path.join(GO, f"traffic_{TAG}.csv"), PROGRAMS, 8192)
+    t.update(traffic(os.path.join(GO, f"traffic_c3_{TAG}.csv"), C3, 16384, "c3/"))
+    json.dump({k: v["total"] for k, v in t.items()}, open(os.path.join(PR, f"traffic_{TAG}.json"), "w"),
               indent=1)
-    ll = read_metrics_csv(os.path.join(GO, "launches_r02.csv"))
+    ll = read_metrics_csv(os.path.join(GO, f"launches_{TAG}.csv"))
     agg = collections.defaultdict(list)
     for name, m in ll:
         agg[short(name)].append(to_us(*m["gpu__time_duration.sum"]))
     tot = sum(sum(v) for v in agg.values())
-    lines = ["# ncu launch list, round r02", "",
+    lines = [f"# ncu launch list, round {TAG}", "",
              "`ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv python "
              "bench.py --steps 1 --warmup 3 --no-c3 --no-c4 --no-c5 --e2e-steps 0 --no-cpu "
-             "--no-unaligned` (raw: `launches_r02.csv`; tools/profile_r02.sh). Cold-cache, "
+             f"--no-unaligned --no-dd137` (raw: `launches_{TAG}.csv`; tools/profile_r02.sh {TAG}). Cold-cache, "
              "serialised: compare shares, not absolutes.", "",
              "| kernel | launches | mean us | share of listed time |", "|---|---:|---:|---:|"]
     for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
         lines.append(f"| {k} | {len(v)} | {sum(v) / len(v):.1f} | {sum(v) / tot:.3f} |")
-    lines += ["", "## DRAM traffic per launch (`traffic_r02.csv`, `traffic_c3_r02.csv`)", "",
+    lines += ["", f"## DRAM traffic per launch (`traffic_{TAG}.csv`, `traffic_c3_{TAG}.csv`)", "",
               "| program | kernel | read GB | write GB | total / algorithmic | us |",
               "|---|---|---:|---:|---:|---:|"]
     for p, v in t.items():
         lines.append(f"| {p} | {v['kernel']} | {v['read'] / 1e9:.3f} | {v['write'] / 1e9:.3f} | "
                      f"{v['total'] / v['algorithmic']:.3f} | {v['us']:.1f} |")
-    open(os.path.join(PR, "launches_r02.md"), "w").write("\n".join(lines) + "\n")
-    os.system(f"cp {os.path.join(GO, 'launches_r02.csv')} {os.path.join(GO, 'traffic_r02.csv')} "
-              f"{os.path.join(GO, 'traffic_c3_r02.csv')} {PR}/")
+    open(os.path.join(PR, f"launches_{TAG}.md"), "w").write("\n".join(lines) + "\n")
+    os.system(f"cp {os.path.join(GO, f'launches_{TAG}.csv')} {os.path.join(GO, f'traffic_{TAG}.csv')} "
+              f"{os.path.join(GO, f'traffic_c3_{TAG}.csv')} {PR}/")
     # full captures: key metrics + stall breakdown + hot SASS
     keys = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
             "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
@@ -72,9 +73,9 @@ def main():
             "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
             "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
             "launch__occupancy_limit_registers", "launch__occupancy_limit_shared_mem"]
-    out = ["# ncu --set full captures, round r02 (tools/profile_r02.sh)", ""]
+    out = [f"# ncu --set full captures, round {TAG} (tools/profile_r02.sh {TAG})", ""]
     for f in sorted(os.listdir(GO)):
-        if not (f.startswith("prof_r02_") and f.endswith(".ncu-rep")):
+        if not (f.startswith(f"prof_{TAG}_") and f.endswith(".ncu-rep")):
             continue
         rep = os.path.join(GO, f)
         raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
@@ -96,7 +97,7 @@ def main():
         hot = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "sass_hot.py"), tmp, "12"],
                              capture_output=True, text=True).stdout
         out += ["", "```", hot.rstrip(), "```", ""]
-    open(os.path.join(PR, "ncu_r02_summary.md"), "w").write("\n".join(out) + "\n")
+    open(os.path.join(PR, f"ncu_{TAG}_summary.md"), "w").write("\n".join(out) + "\n")
     print("wrote", PR)
 
 
