@@ -44,6 +44,8 @@ def main():
     ll = read_metrics_csv(os.path.join(GO, f"launches_{TAG}.csv"))
     agg = collections.defaultdict(list)
     for name, m in ll:
+        if "spin_kernel" in name:  # torch.cuda._sleep before timed groups: not ours
+            continue
         agg[short(name)].append(to_us(*m["gpu__time_duration.sum"]))
     tot = sum(sum(v) for v in agg.values())
     lines = [f"# ncu launch list, round {TAG}", "",
