@@ -464,7 +464,12 @@ def run_gpu(args):
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
-        cpu = cpu_baseline(args, per_ms)
+        # configs[0]: 1024^2 cdf53 Sweldens forward on the GPU, isolated
+        im0 = torch.rand((1024, 1024), device=dev, generator=g, dtype=torch.float32)
+        q0 = torch.empty((4, 512, 512), device=dev, dtype=torch.float32)
+        s0 = wl.build_scheme("sweldens", "cdf53")
+        c0_ms = time_isolated(lambda: wl.forward(im0, s0, out=q0), stream)
+        cpu = cpu_baseline(args, per_ms, c0_ms)
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "GPixel/s", "n_gpus": ws,
@@ -720,12 +725,13 @@ def run_c5(args, wl, ws, rank, peak):
     return out
 
 
-def cpu_baseline(args, gpu_ms):
+def cpu_baseline(args, gpu_ms, c0_gpu_ms=None):
     """The unmodified reference (oracle/_ref) on this host at the FULL
     configs[1] size (n x n, float64) for the headline pair: cdf53 Monolithic
     and cdf97 Monolithic* forward (transform.cpp:163) + the reference inverse
     (transform.cpp:178), next to the GPU's isolated times of the same
-    programs (same size, same input distribution)."""
+    programs (same size, same input distribution); plus configs[0], the
+    reference CLI's bench shape (1024^2 cdf53 Sweldens forward)."""
     try:
         import numpy as np
         ref, kind, cores = _ref_lib()
@@ -747,7 +753,22 @@ def cpu_baseline(args, gpu_ms):
                              "gpu_over_cpu": round(1e3 * t / g_ms, 1) if g_ms else None}
             px += 2 * img.size
             tot += t2 - t0
+        # configs[0]: the reference CLI's bench shape (wavelift_main.cpp:236-272), 1024^2
+        # cdf53 Sweldens forward, median of 5 runs
+        im0 = np.random.default_rng(1).random((1024, 1024))
+        ts = []
+        for _ in range(5):
+            t0 = time.perf_counter()
+            ref.forward(im0, "cdf53", "sweldens", "periodic", False)
+            ts.append(time.perf_counter() - t0)
+        t0s = statistics.median(ts)
+        c0 = {"workload": "configs[0]: cdf53 sweldens single-level forward, 1024x1024 "
+                          "(reference float64 on the host cores vs the GPU float32, isolated)",
+              "cpu_ms": round(1e3 * t0s, 2), "cpu_ns_per_px": round(1e9 * t0s / im0.size, 2),
+              "gpu_ms": round(c0_gpu_ms, 5) if c0_gpu_ms else None,
+              "gpu_over_cpu": round(1e3 * t0s / c0_gpu_ms, 1) if c0_gpu_ms else None}
         return {"value": px / tot / 1e9, "unit": "GPixel/s", "cores": cores, "kind": kind,
+                "configs0": c0,
                 "ns_per_pixel": 1e9 * tot / px, "seconds": round(tot, 2),
                 "sample": f"{n}x{n} float64 (the full configs[1] size), uniform[0,1) numpy seed "
                           f"12345: cdf53 monolithic and cdf97 monolithic_star, forward + "

@@ -1749,9 +1749,12 @@ struct Config<1, 1> {  // cdf97 inverse
 #ifndef WL_CPT137I
 #define WL_CPT137I 2
 #endif
+#ifndef WL_CPT137F
+#define WL_CPT137F 4
+#endif
 template <>
 struct Config<2, 0> {
-    static constexpr int R = WL_R137, NW = WL_NW137, CPT = 4, NS = 2;
+    static constexpr int R = WL_R137, NW = WL_NW137, CPT = WL_CPT137F, NS = 2;
     static constexpr bool XF = false;
     static constexpr int MAXB = 0;
     static constexpr int KR = 2;
