@@ -232,12 +232,6 @@ int wl_dwt2_inverse_host(const float* ll, const float* hl, const float* lh, cons
  * interpreter, 2 = force the fast engine (WL_EINVAL where unsupported).
  * Returns the previous value. Process-global. */
 int wl_set_engine(int engine);
-/* Forward pyramids can run two consecutive levels in one persistent launch
- * where the fast engine can (periodic lifting schemes; the coarser level
- * re-reads the finer LL from L2). 1 = on, 0 = one launch per level (default;
- * environment WL_FUSE=1 turns it on). Results are bit-identical either way.
- * Returns the previous value. Process-global. */
-int wl_set_level_fusion(int on);
 /* Pyramid drivers (wl_dwt2_pyramid_*): a call repeated with identical
  * arguments is replayed from a CUDA graph captured on its second occurrence
  * (one cudaGraphLaunch instead of one launch per level). 1 = on (default;

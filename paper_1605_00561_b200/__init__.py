@@ -82,8 +82,6 @@ def lib() -> ctypes.CDLL:
         l.wl_dwt2_forward_host.argtypes = [fp, i, i, lg, i, i, i, i, fp, fp, fp, fp, lg]
         l.wl_dwt2_inverse_host.argtypes = [fp, fp, fp, fp, i, i, lg, i, i, i, i, fp, lg]
         l.wl_set_engine.argtypes = [i]
-        if hasattr(l, "wl_set_level_fusion"):  # absent in A/B builds of older sources
-            l.wl_set_level_fusion.argtypes = [i]
         l.wl_launch_count.restype = lg
         if hasattr(l, "wl_set_graphs"):
             l.wl_set_graphs.argtypes = [i]
@@ -114,11 +112,6 @@ def version() -> str:
 def set_engine(engine: int) -> int:
     """0 auto, 1 generic tile interpreter, 2 fast register-tile engine."""
     return lib().wl_set_engine(engine)
-
-
-def set_level_fusion(on: bool) -> bool:
-    """Fuse consecutive forward pyramid levels into one launch (default off)."""
-    return bool(lib().wl_set_level_fusion(1 if on else 0))
 
 
 def set_graphs(on: bool) -> bool:

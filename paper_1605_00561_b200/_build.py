@@ -27,8 +27,7 @@ FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
                 "--expt-relaxed-constexpr", "-Xptxas", "-v", "-ccbin", "g++",
                 "-I" + os.path.join(ROOT, "include")] + os.environ.get("WL_DEFS", "").split()
 SOURCES = ["wl_capi.cu", "wl_interp.cu", "wl_fast.cu", "wl_fast_cdf53_fwd.cu",
-           "wl_fast_cdf53_inv.cu", "wl_fast_cdf97_fwd.cu", "wl_fast_cdf97_inv.cu", "wl_fast_cdf53_fused.cu",
-           "wl_fast_cdf97_fused.cu", "wl_conv.cu", "wl_strips.cu", "wl_host.cu", "wl_desc.cu",
+           "wl_fast_cdf53_inv.cu", "wl_fast_cdf97_fwd.cu", "wl_fast_cdf97_inv.cu", "wl_conv.cu", "wl_strips.cu", "wl_host.cu", "wl_desc.cu",
            "wl_fast_cdf53_direct.cu", "wl_fast_cdf97_direct.cu", "wl_fast_dd137_fwd.cu",
            "wl_fast_dd137_inv.cu", "wl_fast_dd137_direct.cu"]
 

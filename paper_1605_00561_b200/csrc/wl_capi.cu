@@ -17,13 +17,6 @@ namespace {
 thread_local std::string g_err;
 std::atomic<long> g_launches{0};
 std::atomic<int> g_engine{0};
-// Fused level pairs in forward pyramids (wl_set_level_fusion; WL_FUSE=1
-// enables). Off by default: measured slower than one launch per level on
-// B200 except for the largest single images ("Fused levels").
-std::atomic<int> g_fuse{[] {
-    const char* v = getenv("WL_FUSE");
-    return v && v[0] == '1' ? 1 : 0;
-}()};
 
 int fail(int code, const std::string& msg) {
     g_err = msg;
@@ -125,7 +118,6 @@ const char* wl_version(void) {
 
 int wl_set_engine(int engine) { return g_engine.exchange(engine); }
 
-int wl_set_level_fusion(int on) { return g_fuse.exchange(on ? 1 : 0); }
 
 long wl_launch_count(void) { return g_launches.load(); }
 
@@ -473,14 +465,12 @@ size_t wl_pyramid_elems(int w, int h, int levels) {
 
 size_t wl_pyramid_scratch_elems(int w, int h, int levels) {
     if (w <= 0 || h <= 0 || levels < 1) return 0;
-    // Two ping-pong LL buffers of the level-1 plane size (+ the task and
-    // row counters of fused level pairs).
-    return 2 * static_cast<size_t>(w / 2) * static_cast<size_t>(h / 2) +
-           (levels > 1 ? wl_fused_ctr_elems(h / 2, 1) : 0);
+    // Two ping-pong LL buffers of the level-1 plane size.
+    return 2 * static_cast<size_t>(w / 2) * static_cast<size_t>(h / 2);
 }
 
 // transform.cpp:198-227: level l transforms the previous level's LL (the
-// batched path with one image: same launches, fused level pairs included).
+// batched path with one image: same launches).
 int wl_dwt2_pyramid_forward(const float* img, int w, int h, int levels, int wavelet, int scheme,
                             int boundary, int scaling, float* pyramid, float* scratch,
                             void* stream) {
@@ -528,10 +518,8 @@ static int pyramid_inverse_impl(const float* pyramid, int w, int h, int levels, 
 size_t wl_pyramid_batch_scratch_elems(int w, int h, int levels, int n) {
     if (w <= 0 || h <= 0 || levels < 1 || n < 1) return 0;
     const size_t q1 = static_cast<size_t>(w / 2) * (h / 2);
-    // LL ping-pong: n*q1 | n*(q1/4 + q1/16) (a fused pair at level 1 writes
-    // LL_1 and LL_2 side by side), then the fused-launch counters
-    return static_cast<size_t>(n) * (q1 + (levels > 1 ? q1 / 4 + q1 / 16 : 0)) +
-           (levels > 1 ? wl_fused_ctr_elems(h / 2, n) : 0);
+    // LL ping-pong: n*q1 (LL of levels 0, 2, ...) | n*q1/4 (levels 1, 3, ...)
+    return static_cast<size_t>(n) * (q1 + (levels > 1 ? q1 / 4 : 0));
 }
 
 // Batched multi_level_forward (transform.cpp:198-227 per image): one launch
@@ -555,8 +543,6 @@ static int pyramid_forward_batch_impl(const float* imgs, int w, int h, long img_
         return fail(WL_EINVAL, "batch stride too small");
     const size_t q1 = static_cast<size_t>(w / 2) * (h / 2);
     float* ping[2] = {scratch, scratch + static_cast<size_t>(n) * q1};
-    unsigned* ctr = reinterpret_cast<unsigned*>(
-        scratch + static_cast<size_t>(n) * (q1 + q1 / 4 + q1 / 16));
     size_t offs[32];  // pyramid offset of level l's HL plane
     {
         size_t off = 0;
@@ -608,30 +594,7 @@ static int pyramid_forward_batch_impl(const float* imgs, int w, int h, long img_
     long src_stride = img_stride;
     int inbuf = -1;  // scratch buffer holding src (-1: the images)
     for (int l = 0; l < levels;) {
-        const int q = inbuf == 0 ? 1 : 0;  // the other buffer
-        // Two levels per launch where the fast engine can fuse them (periodic
-        // lifting forwards): LL_l is re-read from L2 by the same launch. Its
-        // level l+1 must not overwrite level l's input while tiles still read
-        // it: both LL planes go to the buffer that does not hold the input.
-        if (l + 1 < levels && g_engine.load() != 1 && g_fuse.load()) {
-            float *l0, *l1;
-            long s0, s1;
-            const size_t q_l = static_cast<size_t>(n) * (w >> (l + 1)) * (h >> (l + 1));
-            ll_of(l, q, 0, &l0, &s0);
-            if (inbuf < 0) ll_of(l + 1, 1, 0, &l1, &s1);  // level 0 fills buffer 0
-            else ll_of(l + 1, q, q_l, &l1, &s1);
-            const WlLevel L0 = level(l, src, src_stride, l0, s0);
-            const WlLevel L1 = level(l + 1, l0, s0, l1, s1);
-            const cudaError_t e = wl_launch_fast_fused(L0, L1, ctr, s);
-            if (e == cudaSuccess) {
-                src = l1;
-                src_stride = s1;
-                inbuf = inbuf < 0 ? 1 : q;
-                l += 2;
-                continue;
-            }
-            if (e != cudaErrorNotSupported) return cuda_status(e, "fast_kernel (fused levels)");
-        }
+        const int q = inbuf == 0 ? 1 : 0;  // the other buffer (LL_l never overwrites its input)
         float* ll;
         long ls;
         ll_of(l, q, 0, &ll, &ls);
@@ -720,7 +683,7 @@ std::atomic<int> g_graphs{[] {
 }()};
 
 struct GraphKey {
-    int fn, device, engine, fuse;
+    int fn, device, engine, pad;
     int w, h, n, levels, wavelet, scheme, boundary, scaling;
     const void *a, *b, *c;
     long s1, s2;
@@ -769,7 +732,6 @@ int with_graph(GraphKey k, void* stream, F&& run) {
     if (!g_graphs.load()) return run(stream);
     cudaGetDevice(&k.device);
     k.engine = g_engine.load();
-    k.fuse = g_fuse.load();
     GraphCache& c = g_cache;
     GraphEntry* e = c.find(k);
     if (!e) {

@@ -126,13 +126,6 @@ cudaError_t wl_fast_dd137_inv(int scheme, const WlLevel& L, const wlfast::Plan& 
                               cudaStream_t s);
 cudaError_t wl_fast_dd137_direct(int scheme, const WlLevel& L, const wlfast::Plan& p,
                                  cudaStream_t s);
-cudaError_t wl_fast_cdf53_fwd_fused(int scheme, const WlLevel& L0, const wlfast::Plan& p0,
-                                   const WlLevel& L1, const wlfast::Plan& p1, unsigned* ctr,
-                                   cudaStream_t s);
-cudaError_t wl_fast_cdf97_fwd_fused(int scheme, const WlLevel& L0, const wlfast::Plan& p0,
-                                   const WlLevel& L1, const wlfast::Plan& p1, unsigned* ctr,
-                                   cudaStream_t s);
-
 namespace {
 
 template <class C>
@@ -300,32 +293,4 @@ cudaError_t wl_launch_fast(const WlLevel& L, cudaStream_t stream) {
         if (e != cudaSuccess) return e;
     }
     return cudaSuccess;
-}
-
-size_t wl_fused_ctr_elems(int qh0, int nb) {
-    // 2 + nb * R0 words; R0 <= qh0 / TH + 3 with TH >= 22 for every forward geometry
-    return 16 + static_cast<size_t>(nb > 1 ? nb : 1) * (qh0 / 16 + 4);
-}
-
-cudaError_t wl_launch_fast_fused(const WlLevel& L0, const WlLevel& L1, unsigned* ctr,
-                                 cudaStream_t stream) {
-    if (!ctr) return cudaErrorNotSupported;
-    if (L0.direction != 0 || L1.direction != 0 || L0.boundary != 0 || L1.boundary != 0 ||
-        L0.yhi > 0 || L1.yhi > 0 || L0.wavelet != L1.wavelet || L0.scheme != L1.scheme ||
-        L0.nb != L1.nb || L1.qw * 2 != L0.qw || L1.qh * 2 != L0.qh || L1.in[0] != L0.out[0] ||
-        L1.in_pitch != L0.out_pitch || (L0.nb > 1 && L1.in_bstride[0] != L0.out_bstride[0]))
-        return cudaErrorNotSupported;
-    if (wl_host_program(L0.prog).is_conv || L0.wavelet > 1) return cudaErrorNotSupported;
-    if (wl_fast_mode(L0) != 1 || wl_fast_mode(L1) != 1) return cudaErrorNotSupported;
-    int R, NW, CPT, KR;
-    geometry(L0, &R, &NW, &CPT, &KR);
-    const int H = wl_host_program(L0.prog).halo;
-    const wlfast::Plan p0 = wlfast::plan_tiles(L0, H, R, NW, CPT, false, true);
-    const wlfast::Plan p1 = wlfast::plan_tiles(L1, H, R, NW, CPT, false, true);
-    if (!p0.ok || !p1.ok) return cudaErrorNotSupported;
-    const int nb = L0.nb > 1 ? L0.nb : 1;
-    if (2 + static_cast<size_t>(nb) * p0.tiles_y > wl_fused_ctr_elems(L0.qh, nb))
-        return cudaErrorNotSupported;
-    return L0.wavelet == 0 ? wl_fast_cdf53_fwd_fused(L0.scheme, L0, p0, L1, p1, ctr, stream)
-                           : wl_fast_cdf97_fwd_fused(L0.scheme, L0, p0, L1, p1, ctr, stream);
 }

@@ -158,10 +158,6 @@ __device__ __forceinline__ void mbar_wait_backoff(uint64_t* b, unsigned parity) 
 #ifndef WL_PLAN_V2
 #define WL_PLAN_V2 1
 #endif
-// Fused pyramid launches: tasks claimed per atomic.
-#ifndef WL_FUSE_CLAIM
-#define WL_FUSE_CLAIM 4
-#endif
 // Forward input tile as WL_FWD_SPLIT TMA boxes of 2*kRows/WL_FWD_SPLIT rows.
 #ifndef WL_FWD_SPLIT
 #define WL_FWD_SPLIT 1
@@ -278,27 +274,9 @@ static __device__ __noinline__ void wait_halo_flags(const unsigned* fa, const un
     asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
-// Two pyramid levels in ONE persistent launch (forward, periodic). Level-l
-// tiles and level-(l+1) tiles are two task queues (global counters ctr[0],
-// ctr[1], claimed in order). Level-l tiles never wait. A level-(l+1) tile
-// reads LL_l rows that level-l tiles write: each CTA's producer keeps the
-// next level-(l+1) task it claimed pending and takes it as soon as the
-// level-l tile rows its TMA box covers are complete (per-row counts
-// ctr[2 + b*R0 + j]), processing level-l tiles meanwhile -- so LL_l is
-// re-read right after it was written, from L2, and nobody idles while
-// level-l tiles remain (then the pending task is waited for). No cycle:
-// level-l tiles depend on nothing.
-struct FuseArgs {
-    unsigned* ctr;  // [0] level-l claims, [1] level-(l+1) claims, [2 + b*R0 + j] row counts
-    int nb;         // images
-    int R0, R1;     // tile rows per image of level l / l+1
-    int X0n, X1n;   // tile columns
-    int n0, n1;     // tasks per level (all images)
-    unsigned target;  // row count of a finished level-l tile row (X0n * NW)
-};
+// Kernel arguments: one level per launch (lv[0]).
 struct KArgs {
-    FastArgs lv[2];  // lv[1]: the second level of a fused launch
-    FuseArgs fu;
+    FastArgs lv[1];
 };
 
 __device__ __host__ __forceinline__ int floordiv(int a, int b) {
@@ -319,75 +297,6 @@ __device__ __forceinline__ unsigned ld_relaxed_gpu_u32(const unsigned* p) {
     asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
-// Producer of a level-(l+1) tile: are the level-l tile rows holding LL_l
-// rows [2*cy, 2*(cy + rows)) (wrapped) complete? One poll of the (few) row
-// counts with independent loads; on success one acquire fence (plus the
-// generic -> async proxy fence: the tile is read by TMA). `known` caches the
-// last verified row range of an image (tiles of one row share it).
-struct RowCache {
-    int b = -1, lo = 0, hi = -1;
-};
-__device__ inline bool fused_rows_ready(const KArgs& K, int b, int cy, int rows, RowCache& known) {
-    const FastArgs& a0 = K.lv[0];
-    const FuseArgs& f = K.fu;
-    const int qh0 = a0.qh;
-    const int ya = 2 * cy, yb = 2 * (cy + rows);
-    auto jof = [&](int y) { return floordiv(y - a0.Y0, a0.TH) - a0.ty0; };
-    int lo0, hi0, lo1 = 0, hi1 = -1;  // one or two row intervals
-    if (yb - ya >= qh0) {
-        lo0 = 0;
-        hi0 = f.R0 - 1;
-    } else {
-        const int y0 = ((ya % qh0) + qh0) % qh0, y1 = (((yb - 1) % qh0) + qh0) % qh0;
-        if (y0 <= y1) {
-            lo0 = jof(y0);
-            hi0 = jof(y1);
-        } else {
-            lo0 = jof(y0);
-            hi0 = f.R0 - 1;
-            hi1 = jof(y1);
-        }
-    }
-    if (hi1 < 0 && known.b == b && lo0 >= known.lo && hi0 <= known.hi) return true;
-    const unsigned* c = f.ctr + 2 + (size_t)b * f.R0;
-    bool ok = true;
-    for (int j = lo0; j <= hi0; ++j) ok &= ld_relaxed_gpu_u32(c + j) >= f.target;
-    for (int j = lo1; j <= hi1; ++j) ok &= ld_relaxed_gpu_u32(c + j) >= f.target;
-    if (!ok) return false;
-    asm volatile("fence.acq_rel.gpu;" ::: "memory");
-    asm volatile("fence.proxy.async.global;" ::: "memory");
-    if (hi1 < 0) {
-        known.b = b;
-        known.lo = lo0;
-        known.hi = hi0;
-    }
-    return true;
-}
-
-// The (at most kMaxDep) level-l tile rows a level-(l+1) box covers.
-constexpr int kMaxDep = 6;
-__device__ inline int fused_dep_rows(const KArgs& K, int cy, int rows, int (&j)[kMaxDep]) {
-    const FastArgs& a0 = K.lv[0];
-    const int qh0 = a0.qh, R0 = K.fu.R0;
-    const int ya = 2 * cy, yb = 2 * (cy + rows);
-    auto jof = [&](int y) { return floordiv(y - a0.Y0, a0.TH) - a0.ty0; };
-    int n = 0;
-    auto add = [&](int lo, int hi) {
-        for (int q = lo; q <= hi && n < kMaxDep; ++q) j[n++] = q;
-    };
-    if (yb - ya >= qh0) return -1;  // the whole image (tiny levels)
-    const int y0 = ((ya % qh0) + qh0) % qh0, y1 = (((yb - 1) % qh0) + qh0) % qh0;
-    if (y0 <= y1) {
-        if (jof(y1) - jof(y0) >= kMaxDep) return -1;
-        add(jof(y0), jof(y1));
-    } else {
-        if (R0 - jof(y0) + jof(y1) + 1 > kMaxDep) return -1;
-        add(jof(y0), R0 - 1);
-        add(0, jof(y1));
-    }
-    return n;
-}
-
 // Producer back-off cap (ns) per program: the polling producer shares an SM
 // sub-partition with compute warps, so how long it sleeps between polls is
 // a trade-off between refill latency and stolen issue slots. Measured on
@@ -608,24 +517,18 @@ constexpr int xch_comps() {
 // under a column mask; the producer warp exits at once and the stage ring is
 // not allocated. Same instruction sequence per cell, so the same results.
 template <class P, int DIR, int R, int NW, int CPT, int NS, bool XF, bool MIRROR,
-          bool FUSED = false, bool DIRECT = false>
+          bool DIRECT = false>
 __global__ void __launch_bounds__((NW + 1) * 32,
                                   (Geometry<R, NW, CPT, NS, xch_comps<P, XF>(), P::kReach>::kMinBlocks))
     fast_kernel(const __grid_constant__ CUtensorMap m0, const __grid_constant__ CUtensorMap m1,
                 const __grid_constant__ CUtensorMap m2, const __grid_constant__ CUtensorMap m3,
                 const __grid_constant__ KArgs K) {
-    static_assert(!FUSED || (DIR == 0 && !MIRROR), "fused launches: periodic forwards");
-    static_assert(!DIRECT || (!FUSED && !MIRROR), "direct-load launches: plain plans");
-    __shared__ int4 task_sm[NS];  // fused: the task of each stage (producer -> consumers)
-    // fused: per processed tile (ring of kRing), warps done storing / its level-l row
-    constexpr int kRing = 8;
-    static_assert(kRing > NS, "report ring");
-    __shared__ unsigned done_cnt[kRing];
-    __shared__ int row_ring[kRing];
+    static_assert(!DIRECT || !MIRROR, "direct-load launches: plain plans");
+    __shared__ int4 task_sm[NS];  // dynamic claims: the tile of each stage (producer -> consumers)
     constexpr int NXC = xch_comps<P, XF>();
     constexpr int KR = P::kReach;  // ghost rows / neighbour cells a step reads
     static_assert(R >= 2 * KR && KR <= CPT, "edge rows / lane-neighbour cells");
-    static_assert(KR == 1 || (!MIRROR && !FUSED), "reach-2 programs: plain / direct plans");
+    static_assert(KR == 1 || !MIRROR, "reach-2 programs: plain / direct plans");
     using G = Geometry<R, NW, CPT, NS, NXC, KR>;
     constexpr int H = P::kHalo;
     constexpr int TWC = G::TWC;
@@ -653,8 +556,6 @@ __global__ void __launch_bounds__((NW + 1) * 32,
             mbar_init(&full[k], 1);
             mbar_init(&empty[k], NW * 32);
         }
-        if (FUSED)
-            for (int k = 0; k < kRing; ++k) done_cnt[k] = 0;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -666,170 +567,7 @@ __global__ void __launch_bounds__((NW + 1) * 32,
     if (warp == NW) {
         // ---------------- producer warp: TMA tile stream ----------------
         if constexpr (DIRECT) return;  // compute warps load their own cells
-        if (FUSED && lane == 0) {
-            const FuseArgs& f = K.fu;
-            // Level-l tasks are claimed in chunks of kClaim, the next chunk one
-            // chunk ahead (the claim's round trip never stalls the TMA stream);
-            // level-(l+1) tasks one at a time, also one ahead.
-            constexpr int kClaim = WL_FUSE_CLAIM;
-            int base = atomicAdd(f.ctr, kClaim), k_in = 0;
-            int next = atomicAdd(f.ctr, kClaim);
-            int p1 = atomicAdd(f.ctr + 1, 1);   // pending level-(l+1) task
-            int p1n = atomicAdd(f.ctr + 1, 1);  // the one after it
-            RowCache known;
-            // Completion reports of level-l tile rows: the compute warps count
-            // their finished stores per tile in shared memory (release.cta);
-            // this thread turns them, in order, into per-row global counts
-            // (one GPU-scope fence per run of tiles of one row) -- the fence's
-            // wait for outstanding stores is taken here, not by compute warps.
-            int sig = 0, prow = -1;
-            unsigned pcnt = 0;
-            auto flush = [&]() {
-                if (prow >= 0) {
-                    asm volatile("fence.acq_rel.gpu;" ::: "memory");
-                    asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(
-                                     f.ctr + 2 + prow), "r"(pcnt) : "memory");
-                    prow = -1;
-                    pcnt = 0;
-                }
-            };
-            auto report = [&](int upto, bool wait) {  // tiles [sig, upto)
-                while (sig < upto) {
-                    const int sl = sig & (kRing - 1);
-                    unsigned c;
-                    asm volatile("ld.acquire.cta.shared.u32 %0, [%1];"
-                                 : "=r"(c) : "r"(smem_u32(&done_cnt[sl])) : "memory");
-                    if (c < NW) {
-                        if (!wait) return;
-                        __nanosleep(32);
-                        continue;
-                    }
-                    done_cnt[sl] = 0;
-                    const int row = row_ring[sl];
-                    if (row >= 0) {
-                        if (row != prow) flush();
-                        prow = row;
-                        pcnt += NW;
-                    }
-                    ++sig;
-                }
-            };
-            int issued = 0;
-            auto wait_empty = [&](int s_, unsigned ph) {
-                unsigned ns = 32;
-                for (int polls = 0; !mbar_test(&empty[s_], ph); ++polls) {
-                    report(issued, false);
-                    if (polls > 4) flush();
-                    __nanosleep(ns);
-                    ns = ns < WL_PROD_BACKOFF_NS ? 2 * ns : WL_PROD_BACKOFF_NS;
-                }
-            };
-            // level-(l+1) task -> image, tile row (list order k = 1..R1-1, 0), column, box row
-            const FastArgs& a1 = K.lv[1];
-            auto decode1 = [&](int t1, int& b_, int& k_, int& tx_, int& cy_) {
-                const int per = f.R1 * f.X1n;
-                b_ = t1 / per;
-                const int r = t1 - b_ * per, i1 = r / f.X1n;
-                k_ = i1 + 1 < f.R1 ? i1 + 1 : 0;
-                tx_ = r - i1 * f.X1n;
-                cy_ = a1.Y0 + (k_ + a1.ty0) * a1.TH - H - 1;
-            };
-            int pb = 0, pk = 0, ptx = 0, pcy = 0;
-            // the pending task's row counts are loaded one iteration ahead
-            // (their round trip overlaps the TMA issue and the stage wait)
-            int pj[kMaxDep], pn = 0;
-            unsigned pv[kMaxDep];
-            auto set_pending = [&]() {
-                decode1(p1, pb, pk, ptx, pcy);
-                pn = fused_dep_rows(K, pcy, G::kRows, pj);
-            };
-            auto prefetch = [&]() {
-                const unsigned* c = f.ctr + 2 + (size_t)pb * f.R0;
-#pragma unroll
-                for (int q = 0; q < kMaxDep; ++q)
-                    if (q < pn) pv[q] = ld_relaxed_gpu_u32(c + pj[q]);
-            };
-            auto prefetched_ready = [&]() {
-                if (pn < 0) return fused_rows_ready(K, pb, pcy, G::kRows, known);
-                bool ok = true;
-#pragma unroll
-                for (int q = 0; q < kMaxDep; ++q)
-                    if (q < pn) ok &= pv[q] >= f.target;
-                if (ok) {
-                    asm volatile("fence.acq_rel.gpu;" ::: "memory");
-                    asm volatile("fence.proxy.async.global;" ::: "memory");
-                }
-                return ok;
-            };
-            if (p1 < f.n1) {
-                set_pending();
-                prefetch();
-            }
-            for (int i = 0;; ++i) {
-                const int s = i % NS;
-                const unsigned use = i / NS;
-                int lvl, b, tyi, txi;
-                const int t0 = base + k_in;
-                bool take1 = p1 < f.n1 && prefetched_ready();
-                if (!take1 && t0 >= f.n0 && p1 < f.n1) {
-                    // no level-l work left: wait for the pending task's rows
-                    unsigned ns = 32;
-                    while (!fused_rows_ready(K, pb, pcy, G::kRows, known)) {
-                        report(issued, false);  // this CTA's own rows may be missing
-                        flush();
-                        __nanosleep(ns);
-                        ns = ns < 256 ? 2 * ns : 256;
-                    }
-                    take1 = true;
-                }
-                if (take1) {
-                    lvl = 1;
-                    b = pb;
-                    tyi = pk;
-                    txi = ptx;
-                    p1 = p1n;
-                    if (p1 < f.n1) {
-                        set_pending();
-                        p1n = atomicAdd(f.ctr + 1, 1);
-                    }
-                } else if (t0 < f.n0) {
-                    lvl = 0;
-                    const int per = f.R0 * f.X0n;
-                    b = t0 / per;
-                    const int r = t0 - b * per;
-                    tyi = r / f.X0n;
-                    txi = r - tyi * f.X0n;
-                    if (++k_in == kClaim) {
-                        base = next;
-                        k_in = 0;
-                        if (base < f.n0) next = atomicAdd(f.ctr, kClaim);
-                    }
-                } else {  // both queues drained
-                    if (i >= NS) wait_empty(s, (use - 1) & 1);
-                    task_sm[s] = make_int4(-1, 0, 0, 0);
-                    mbar_arrive(&full[s]);  // consumers see the sentinel and stop
-                    report(issued, true);
-                    flush();
-                    break;
-                }
-                const FastArgs& a = K.lv[lvl];
-                const int cx = tile_xs(a, txi + a.tx0) - HX;
-                const int cy = tile_ys(a, tyi + a.ty0) - H - KR;
-                if (i >= NS) wait_empty(s, (use - 1) & 1);
-                report(i - kRing + 1, true);  // ring slot i % kRing is free
-                row_ring[i & (kRing - 1)] = lvl == 0 ? b * f.R0 + tyi : -1;
-                issued = i + 1;
-                task_sm[s] = make_int4(lvl, b, tyi, txi);
-                float* dst = stage + s * G::kStageFloats;
-                mbar_expect_tx(&full[s], G::kStageBytes);
-                constexpr int kSplitRows = 2 * G::kRows / WL_FWD_SPLIT;
-#pragma unroll
-                for (int q = 0; q < WL_FWD_SPLIT; ++q)
-                    tma_load_3d(dst + q * kSplitRows * 2 * TWC, lvl ? &m1 : &m0, &full[s], 2 * cx,
-                                2 * cy + q * kSplitRows, b);
-                if (p1 < f.n1) prefetch();
-            }
-        } else if (lane == 0 && a.sched) {
+        if (lane == 0 && a.sched) {
             // Dynamic tile claims: the first tile is blockIdx.x, every further
             // one comes from a global counter, so CTAs on SMs that run ahead
             // take more tiles and the launch's tail shrinks (static round robin
@@ -951,25 +689,14 @@ __global__ void __launch_bounds__((NW + 1) * 32,
     }
 
     // ---------------- compute warps ----------------
-    // Fused launches: a warp reports a level-l tile row done (ctr += 1,
-    // release) one tile later, right before its next stores, when its
-    // previous stores have long drained -- the fence then costs nothing.
     float v[R][CPT][4];
     float gu[KR][CPT][4], gd[KR][CPT][4];  // KR ghost rows above / below
     int xslot = 0;
 
     for (int i = 0, t = blockIdx.x;; t += gridDim.x) {
         const int s = i % NS;
-        int b, tyi, txi, lvl = 0;
-        if constexpr (FUSED) {
-            mbar_wait(&full[s], (i / NS) & 1);
-            const int4 tk = task_sm[s];
-            if (tk.x < 0) break;
-            lvl = tk.x;
-            b = tk.y;
-            tyi = tk.z;
-            txi = tk.w;
-        } else {
+        int b, tyi, txi;
+        {
             const FastArgs& a0 = K.lv[0];
             if (!DIRECT && a0.sched) {  // dynamic claims: the producer names the tile
                 mbar_wait(&full[s], (i / NS) & 1);
@@ -1005,7 +732,7 @@ __global__ void __launch_bounds__((NW + 1) * 32,
             // the distance-1 ghosts are overwritten with their mirror images.
             const bool mtile = MIRROR && a.mirror && border;
             const int gy0m = cy + KR + warp * R;  // image row of v[0]
-            if constexpr (!FUSED && !DIRECT)
+            if constexpr (!DIRECT)
                 if (!a.sched) mbar_wait(&full[s], phase);  // (dynamic: waited for the task)
 #ifdef WL_DIAG_TIMES
             if (dg && threadIdx.x == 0 && diag_tiles++ == 0) dg[1] = gtime();
@@ -1156,7 +883,7 @@ __global__ void __launch_bounds__((NW + 1) * 32,
             }
 
             // pair mode: the state as packed pairs A = (c0, c2), B = (c1, c3)
-            constexpr bool PM = PairMode<P>::on && CPT == 4 && !MIRROR && !FUSED && KR == 1;
+            constexpr bool PM = PairMode<P>::on && CPT == 4 && !MIRROR && KR == 1;
             wl2 v2[PM ? R : 1][2][4], gu2[2][4], gd2[2][4];
             if constexpr (PM) {
                 auto pack = [&](const float (&src)[CPT][4], wl2 (&dst)[2][4]) {
@@ -1584,20 +1311,8 @@ __global__ void __launch_bounds__((NW + 1) * 32,
                 }
             }
             }  // CPT == 2
-            if constexpr (FUSED) {  // this warp's stores of tile i-1 are issued: count it
-                __syncwarp();
-                if (lane == 0)
-                    asm volatile("red.release.cta.shared.add.u32 [%0], 1;" ::"r"(
-                                     smem_u32(&done_cnt[(i - 1) & (kRing - 1)]))
-                                 : "memory");
-            }
         };
-        if constexpr (FUSED) {
-            if (lvl) body(std::integral_constant<int, 1>{});
-            else body(std::integral_constant<int, 0>{});
-        } else {
-            body(std::integral_constant<int, 0>{});
-        }
+        body(std::integral_constant<int, 0>{});
     }
 #ifdef WL_DIAG_TIMES
     if (dg && threadIdx.x == 0) {
@@ -1878,8 +1593,8 @@ struct Plan {
 //    [ylo, yhi) only; the rows around them are halo rows physically present
 //    in the buffer (ylo >= H + 1 and yhi <= qh - H - 1 keep every stored
 //    cell's dependency cone and the tiles' ghost rows inside the buffer).
-//  * periodic plans (whole image or strip window) other than the fused
-//    launches' (`legacy`): tile (0, 0) stores cell (0, 0) onwards -- only its
+//  * periodic plans (whole image or strip window; `legacy` = the former grid,
+//    an A/B knob): tile (0, 0) stores cell (0, 0) onwards -- only its
 //    reach + 1 ghost rows / halo columns wrap -- and the last tile row /
 //    column is clamped to end at the image edge (overlapping its neighbour,
 //    which writes the same values), so no tile computes wrapped cells it does
@@ -2003,8 +1718,7 @@ inline Plan plan_tiles(const WlLevel& L, int H, int R, int NW, int CPT, bool no_
     return p;
 }
 
-// Kernel arguments and tensor maps of one level (shared by launch and
-// launch_fused).
+// Kernel arguments and tensor maps of one level.
 template <class P, int DIR, int R, int NW, int CPT, int NS, bool XF>
 bool level_args(const WlLevel& L, const Plan& plan, FastArgs& a, CUtensorMap (&maps)[4]) {
     using G = Geometry<R, NW, CPT, NS, xch_comps<P, XF>(), P::kReach>;
@@ -2125,7 +1839,7 @@ cudaError_t launch_direct(const WlLevel& L, const Plan& plan, cudaStream_t strea
     a.scale = wl_host_program(L.prog).scale;
     a.filter = 0;
     constexpr size_t smem = (size_t)G::kXchFloats * 4 + 16 * NS;
-    auto kern = fast_kernel<P, DIR, R, NW, CPT, NS, XF, false, false, true>;
+    auto kern = fast_kernel<P, DIR, R, NW, CPT, NS, XF, false, true>;
     static int cap[64] = {};
     int dev = 0;
     cudaGetDevice(&dev);
@@ -2143,53 +1857,6 @@ cudaError_t launch_direct(const WlLevel& L, const Plan& plan, cudaStream_t strea
                                 none, none, k);
     wl_count_launch();
     return le != cudaSuccess ? le : cudaGetLastError();
-}
-
-// Fused launch of two consecutive periodic forward levels (L1 reads L0's LL
-// output). `ctr` = wl_fused_ctr_elems(...) words (zeroed here, on the stream).
-// Returns cudaErrorNotSupported when the pair does not qualify.
-template <class P, int DIR, int R, int NW, int CPT, int NS, bool XF, int MAXB>
-cudaError_t launch_fused(const WlLevel& L0, const Plan& p0, const WlLevel& L1, const Plan& p1,
-                         unsigned* ctr, cudaStream_t stream) {
-    if constexpr (DIR != 0) {
-        return cudaErrorNotSupported;
-    } else {
-        constexpr int NXC = xch_comps<P, XF>();
-        using G = Geometry<R, NW, CPT, NS, NXC, P::kReach>;
-        CUtensorMap maps0[4], maps1[4];
-        KArgs k{};
-        if (!level_args<P, DIR, R, NW, CPT, NS, XF>(L0, p0, k.lv[0], maps0) ||
-            !level_args<P, DIR, R, NW, CPT, NS, XF>(L1, p1, k.lv[1], maps1))
-            return cudaErrorInvalidValue;
-        if (k.lv[0].mirror || k.lv[1].mirror || !k.lv[0].wrap || !k.lv[1].wrap ||
-            k.lv[0].Y0 != k.lv[1].Y0 || k.lv[0].TH != k.lv[1].TH || k.lv[0].ty0 != k.lv[1].ty0)
-            return cudaErrorNotSupported;
-        FuseArgs& f = k.fu;
-        const int nb = L0.nb > 1 ? L0.nb : 1;
-        f.ctr = ctr;
-        f.nb = nb;
-        f.R0 = p0.tiles_y;
-        f.R1 = p1.tiles_y;
-        f.X0n = p0.args.tiles_x;
-        f.X1n = p1.args.tiles_x;
-        if ((long)nb * f.R0 * f.X0n >= (1l << 30) || (long)nb * f.R1 * f.X1n >= (1l << 30))
-            return cudaErrorNotSupported;
-        f.n0 = nb * f.R0 * f.X0n;
-        f.n1 = nb * f.R1 * f.X1n;
-        f.target = (unsigned)f.X0n * NW;
-        static int cap[64] = {};
-        auto kern = fast_kernel<P, DIR, R, NW, CPT, NS, XF, false, true>;
-        const int mb = grid_cap<R, NW, CPT, NS, NXC, MAXB, P::kReach>(kern, cap);
-        const int ntasks = f.n0 + f.n1;
-        const int grid = ntasks < mb ? ntasks : mb;
-        cudaError_t e = cudaMemsetAsync(ctr, 0, (2 + (size_t)nb * f.R0) * sizeof(unsigned), stream);
-        if (e != cudaSuccess) return e;
-        // maps: m0 = level-l image, m1 = level-(l+1) input (= LL_l)
-        cudaError_t le = launch_pdl(kern, dim3(grid), dim3((NW + 1) * 32), G::kSmemBytes, stream,
-                                    maps0[0], maps1[0], maps0[0], maps0[0], k);
-        wl_count_launch();
-        return le != cudaSuccess ? le : cudaGetLastError();
-    }
 }
 
 }  // namespace wlfast

@@ -63,12 +63,6 @@ bool wl_fast_supported(const WlLevel& L);
 int wl_fast_mode(const WlLevel& L);
 // wl_set_engine's value (0 auto, 1 interpreter, 2 fast, 3 fast direct-load).
 int wl_engine();
-// Two consecutive periodic forward pyramid levels (L1 reads L0's LL) in one
-// persistent launch; cudaErrorNotSupported when the pair does not qualify
-// (then launch them one by one). `ctr`: wl_fused_ctr_elems(L0.qh, nb) words.
-size_t wl_fused_ctr_elems(int qh0, int nb);
-cudaError_t wl_launch_fast_fused(const WlLevel& L0, const WlLevel& L1, unsigned* ctr,
-                                 cudaStream_t stream);
 
 void wl_count_launch();
 // Diagnostic per-CTA timestamps (WL_DIAG_TIMES builds; wl_diag_set)

@@ -111,7 +111,6 @@ def test_new_entry_points_validate_without_gpu():
     assert st == wl.WL_EINVAL and b"even" in lib.wl_last_error()
     st = lib.wl_dwt2_inverse_host(None, fp, fp, fp, 4, 4, 4, 0, 0, 0, 0, fp, 8)
     assert st == wl.WL_EINVAL and b"null" in lib.wl_last_error()
-    # ping-pong LL planes + the task / row counters of fused level pairs
-    ctr = 16 + 3 * (32 // 16 + 4)
-    assert lib.wl_pyramid_batch_scratch_elems(64, 64, 2, 3) == 3 * (32 * 32 + 16 * 16 + 8 * 8) + ctr
+    # ping-pong LL planes: level-1-size and level-2-size planes per image
+    assert lib.wl_pyramid_batch_scratch_elems(64, 64, 2, 3) == 3 * (32 * 32 + 16 * 16)
     assert lib.wl_pyramid_batch_scratch_elems(64, 64, 1, 3) == 3 * 32 * 32

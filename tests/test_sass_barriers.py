@@ -20,8 +20,8 @@ CUOBJDUMP = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
 
 def barrier_counts(lib_path):
     """{(wavelet, scheme, dir, mangled name): BAR count} for every fast
-    kernel -- each program has a plain and a symmetric-border (mirroring)
-    instantiation, forwards also a fused two-level one, checked separately."""
+    kernel -- each program has a plain, a symmetric-border (mirroring) and a
+    direct-load instantiation, checked separately."""
     out = subprocess.run([CUOBJDUMP, "-sass", lib_path], capture_output=True, text=True,
                          check=True).stdout
     counts, fn = {}, None
@@ -46,26 +46,22 @@ def test_sass_barriers_equal_count_barriers():
     # cdf53 / cdf97: 9 lifting schemes x 2 directions; dd137: 7 (Polyphase(*)
     # stays on the interpreter)
     assert len(programs) == 2 * 9 * 2 + 7 * 2, sorted(programs)
-    # cdf53 / cdf97: plain + mirroring + direct-load variant, forwards also the
-    # fused two-level variant; dd137 (reach 2): plain + direct-load
-    assert len(counts) == 3 * 36 + 18 + 2 * 14, len(counts)
-    kinds = {"direct": 0, "fused": 0}
+    # cdf53 / cdf97: plain + mirroring + direct-load variant; dd137 (reach 2):
+    # plain + direct-load
+    assert len(counts) == 3 * 36 + 2 * 14, len(counts)
+    kinds = {"direct": 0, "mirror": 0}
     for (w, s, d, name), n in counts.items():
         want = wl.build_scheme(s, w).info(0 if d == "fwd" else 1)["barriers"]
-        xf, mirror, fused, direct = variant_flags(name)
-        if fused:
-            # fused two-level variant: the tile body is instantiated once per
-            # level (one runs per tile), after the one data-availability barrier
-            want = 1 + 2 * (want - 1)
-            kinds["fused"] += 1
+        xf, mirror, direct = variant_flags(name)
         kinds["direct"] += direct
+        kinds["mirror"] += mirror
         assert n == want, (w, s, d, n, want)
-    assert kinds == {"direct": 36 + 14, "fused": 18}, kinds
+    assert kinds == {"direct": 36 + 14, "mirror": 36}, kinds
 
 
 def variant_flags(name):
-    """(XF, MIRROR, FUSED, DIRECT) template flags of a mangled fast_kernel."""
-    m = re.search(r"Lb(\d)ELb(\d)ELb(\d)ELb(\d)EEEv14CUtensorMap", name)
+    """(XF, MIRROR, DIRECT) template flags of a mangled fast_kernel."""
+    m = re.search(r"Lb(\d)ELb(\d)ELb(\d)EEEv14CUtensorMap", name)
     assert m, name
     return tuple(int(x) for x in m.groups())
 
@@ -85,6 +81,4 @@ def test_broken_barrier_variant_drops_one_barrier():
         want = wl.build_scheme(s, w).info(0 if d == "fwd" else 1)["barriers"]
         # epoch 1 exists only for schemes with >= 2 barriers
         want = want - 1 if want >= 2 else want
-        if variant_flags(name)[2]:
-            want = 1 + 2 * (want - 1)  # fused variant: one body per level
         assert n == want, (w, s, d, n, want)

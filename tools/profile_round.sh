@@ -21,7 +21,4 @@ cap c3_cdf97_mono_star_inv cdf97 monolithic_star inv 16384
 cap c3_cdf53_mono_fwd cdf53 monolithic fwd 16384
 cap c3_cdf53_mono_inv cdf53 monolithic inv 16384
 cap bench_cdf97_polyphase_inv cdf97 polyphase inv 8192
-# fused two-level pyramid launch (opt-in path): 32 x 4096^2, cdf53 Monolithic*
-WL_FUSE=1 ncu --set full --import-source on --clock-control none -k regex:fast_kernel -s 2 -c 1 \
-    -o $O/prof_${TAG}_fused_cdf53_batch python tools/prof_fused.py cdf53 4096 32 1 > /dev/null 2>&1
 ls -la $O

@@ -1,5 +1,5 @@
-"""Small fast-engine workload (incl. the fused two-level launch) for
-compute-sanitizer racecheck / synccheck:
+"""Small fast-engine workload (incl. dynamic tile claims and the reach-2
+dd137 kernels) for compute-sanitizer racecheck / synccheck:
 python tools/race_workload.py  (WL_LIB selects the library variant)."""
 import os
 import sys
@@ -16,12 +16,16 @@ for w, s in (("cdf53", "sweldens"), ("cdf97", "monolithic_star")):
     for b in ("periodic", "symmetric"):  # symmetric: interior + mirroring border kernels
         q = wl.forward(img, sch, b)
         wl.inverse(q, w, b, scheme=s)
-# fused two-level pyramid launch (shared-memory task / completion hand-off)
-if hasattr(wl.lib(), "wl_set_level_fusion"):
-    wl.set_level_fusion(True)
-    imgs = torch.rand((2, 128, 256), device="cuda")
-    for w, s in (("cdf53", "sweldens"), ("cdf97", "monolithic_star")):
-        wl.multi_level_forward_batch(imgs, wl.build_scheme(s, w), 2)
-    wl.set_level_fusion(False)
+# more tiles than resident CTAs: the dynamic tile claims (producer -> compute
+# warps task hand-off through shared memory) of the cdf53 / cdf97 inverse kernels
+big = torch.rand((512, 4096), device="cuda")
+for w, s in (("cdf53", "monolithic"), ("cdf97", "sweldens")):
+    sch = wl.build_scheme(s, w)
+    q = wl.forward(big, sch)
+    wl.inverse(q, w, scheme=s)
+# reach-2 dd137 kernels (two ghost rows, two-row edge exchange)
+for s in ("sweldens", "monolithic_star"):
+    q = wl.forward(img, wl.build_scheme(s, "dd137"))
+    wl.inverse(q, "dd137", scheme=s)
 torch.cuda.synchronize()
 print("workload done")
