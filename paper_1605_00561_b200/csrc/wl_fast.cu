@@ -4,6 +4,7 @@
 #include <cstdint>
 #include <cstdlib>
 #include <mutex>
+#include <type_traits>
 
 #include "wl_fast_impl.cuh"
 
@@ -138,30 +139,36 @@ void geo(int* R, int* NW, int* CPT, int* KR) {
 
 // Tile geometry of the instantiation that serves (wavelet, scheme, direction)
 // -- must match the SchemeConfig the kernel was compiled with.
-template <int W, int D>
+template <int W, int D, bool DIRECT, int S>
+using CfgOf = std::conditional_t<DIRECT, wlfast::DirectConfigOf<W, D, S>, wlfast::SchemeConfig<W, D, S>>;
+template <int W, int D, bool DIRECT>
 void geo_wd(int scheme, int* R, int* NW, int* CPT, int* KR) {
-    using namespace wlfast;
     switch (scheme) {
-        case 0: return geo<SchemeConfig<W, D, 0>>(R, NW, CPT, KR);
-        case 1: return geo<SchemeConfig<W, D, 1>>(R, NW, CPT, KR);
-        case 2: return geo<SchemeConfig<W, D, 2>>(R, NW, CPT, KR);
-        case 3: return geo<SchemeConfig<W, D, 3>>(R, NW, CPT, KR);
-        case 4: return geo<SchemeConfig<W, D, 4>>(R, NW, CPT, KR);
-        case 5: return geo<SchemeConfig<W, D, 5>>(R, NW, CPT, KR);
-        case 6: return geo<SchemeConfig<W, D, 6>>(R, NW, CPT, KR);
-        case 7: return geo<SchemeConfig<W, D, 7>>(R, NW, CPT, KR);
-        default: return geo<SchemeConfig<W, D, 8>>(R, NW, CPT, KR);
+        case 0: return geo<CfgOf<W, D, DIRECT, 0>>(R, NW, CPT, KR);
+        case 1: return geo<CfgOf<W, D, DIRECT, 1>>(R, NW, CPT, KR);
+        case 2: return geo<CfgOf<W, D, DIRECT, 2>>(R, NW, CPT, KR);
+        case 3: return geo<CfgOf<W, D, DIRECT, 3>>(R, NW, CPT, KR);
+        case 4: return geo<CfgOf<W, D, DIRECT, 4>>(R, NW, CPT, KR);
+        case 5: return geo<CfgOf<W, D, DIRECT, 5>>(R, NW, CPT, KR);
+        case 6: return geo<CfgOf<W, D, DIRECT, 6>>(R, NW, CPT, KR);
+        case 7: return geo<CfgOf<W, D, DIRECT, 7>>(R, NW, CPT, KR);
+        default: return geo<CfgOf<W, D, DIRECT, 8>>(R, NW, CPT, KR);
     }
 }
 
-void geometry(const WlLevel& L, int* R, int* NW, int* CPT, int* KR) {
+// Tile geometry of the instantiation that serves L (TMA or direct-load).
+template <bool DIRECT>
+void geometry_of(const WlLevel& L, int* R, int* NW, int* CPT, int* KR) {
     const bool f = L.direction == 0;
     if (L.wavelet == 0)
-        f ? geo_wd<0, 0>(L.scheme, R, NW, CPT, KR) : geo_wd<0, 1>(L.scheme, R, NW, CPT, KR);
+        f ? geo_wd<0, 0, DIRECT>(L.scheme, R, NW, CPT, KR) : geo_wd<0, 1, DIRECT>(L.scheme, R, NW, CPT, KR);
     else if (L.wavelet == 1)
-        f ? geo_wd<1, 0>(L.scheme, R, NW, CPT, KR) : geo_wd<1, 1>(L.scheme, R, NW, CPT, KR);
+        f ? geo_wd<1, 0, DIRECT>(L.scheme, R, NW, CPT, KR) : geo_wd<1, 1, DIRECT>(L.scheme, R, NW, CPT, KR);
     else
-        f ? geo_wd<2, 0>(L.scheme, R, NW, CPT, KR) : geo_wd<2, 1>(L.scheme, R, NW, CPT, KR);
+        f ? geo_wd<2, 0, DIRECT>(L.scheme, R, NW, CPT, KR) : geo_wd<2, 1, DIRECT>(L.scheme, R, NW, CPT, KR);
+}
+void geometry(const WlLevel& L, int* R, int* NW, int* CPT, int* KR) {
+    geometry_of<false>(L, R, NW, CPT, KR);
 }
 
 // Programs the fast engine serves: cdf53 / cdf97 lifting schemes, and the
@@ -228,6 +235,7 @@ int wl_fast_mode(const WlLevel& L) {
     const bool force_direct = wl_engine() == 3;
     if (!force_direct && tma_ok(L, CPT) && wlfast::plan_tiles(L, H, R, NW, CPT, false, false, KR).ok)
         return 1;
+    geometry_of<true>(L, &R, &NW, &CPT, &KR);
     if (direct_ok(L) && wlfast::plan_tiles(L, H, R, NW, CPT, true, false, KR).ok) return 2;
     return 0;
 }
@@ -238,7 +246,10 @@ cudaError_t wl_launch_fast(const WlLevel& L, cudaStream_t stream) {
     const int mode = wl_fast_mode(L);
     if (!mode) return cudaErrorNotSupported;
     int R, NW, CPT, KR;
-    geometry(L, &R, &NW, &CPT, &KR);
+    if (mode == 2)
+        geometry_of<true>(L, &R, &NW, &CPT, &KR);
+    else
+        geometry(L, &R, &NW, &CPT, &KR);
     const int H = wl_host_program(L.prog).halo;
     const wlfast::Plan plan = wlfast::plan_tiles(L, H, R, NW, CPT, mode == 2, false, KR);
     cudaError_t e;

@@ -6,12 +6,12 @@ cudaError_t wl_fast_cdf97_direct(int scheme, const WlLevel& L, const wlfast::Pla
                                cudaStream_t s) {
 #define WL_CASE(wi, si, d, P)                                                               \
     case si:                                                                                \
-        return wlfast::launch_direct<P, d, wlfast::SchemeConfig<wi, d, si>::R,              \
-                                     wlfast::SchemeConfig<wi, d, si>::NW,                   \
-                                     wlfast::SchemeConfig<wi, d, si>::CPT,                  \
-                                     wlfast::SchemeConfig<wi, d, si>::NS,                   \
-                                     wlfast::SchemeConfig<wi, d, si>::XF,                   \
-                                     wlfast::SchemeConfig<wi, d, si>::MAXB>(L, p, s);
+        return wlfast::launch_direct<P, d, wlfast::DirectConfigOf<wi, d, si>::R,              \
+                                     wlfast::DirectConfigOf<wi, d, si>::NW,                   \
+                                     wlfast::DirectConfigOf<wi, d, si>::CPT,                  \
+                                     wlfast::DirectConfigOf<wi, d, si>::NS,                   \
+                                     wlfast::DirectConfigOf<wi, d, si>::XF,                   \
+                                     wlfast::DirectConfigOf<wi, d, si>::MAXB>(L, p, s);
     if (L.direction == 0) {
         switch (scheme) {
             WL_FAST_FOREACH_1_0(WL_CASE)

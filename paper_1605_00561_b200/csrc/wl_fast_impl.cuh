@@ -510,6 +510,29 @@ constexpr int xch_comps() {
     }
 }
 
+// Direct-load variant: no stage ring (shared memory holds only the edge
+// exchange), so its occupancy is set by registers: shorter warp rows
+// (WL_DIRECT_R, at least 2 x reach; DirectConfig) and WL_DIRECT_MINB CTAs per
+// SM let a second CTA's loads overlap the first one's compute.
+#ifndef WL_DIRECT_R
+#define WL_DIRECT_R 4
+#endif
+#ifndef WL_DIRECT_MINB
+#define WL_DIRECT_MINB 2
+#endif
+template <class P>
+struct DirectMinBlocks {  // reach-2 rows and the 126-MAC cdf97 Polyphase epochs need
+    static constexpr int value = P::kReach > 1 ? 1 : WL_DIRECT_MINB;  // their registers
+};
+template <>
+struct DirectMinBlocks<P_cdf97_polyphase_fwd> {
+    static constexpr int value = 1;
+};
+template <>
+struct DirectMinBlocks<P_cdf97_polyphase_inv> {
+    static constexpr int value = 1;
+};
+
 // DIRECT: no TMA -- shapes whose pitches/pointers/widths the TMA boxes and
 // the aligned float4 stores cannot take (e.g. 8190^2 images: 32760-byte rows,
 // odd plane widths). Every tile loads its cells with coalesced per-lane
@@ -519,7 +542,8 @@ constexpr int xch_comps() {
 template <class P, int DIR, int R, int NW, int CPT, int NS, bool XF, bool MIRROR,
           bool DIRECT = false>
 __global__ void __launch_bounds__((NW + 1) * 32,
-                                  (Geometry<R, NW, CPT, NS, xch_comps<P, XF>(), P::kReach>::kMinBlocks))
+                                  (DIRECT ? DirectMinBlocks<P>::value
+                                          : Geometry<R, NW, CPT, NS, xch_comps<P, XF>(), P::kReach>::kMinBlocks))
     fast_kernel(const __grid_constant__ CUtensorMap m0, const __grid_constant__ CUtensorMap m1,
                 const __grid_constant__ CUtensorMap m2, const __grid_constant__ CUtensorMap m3,
                 const __grid_constant__ KArgs K) {
@@ -1491,6 +1515,14 @@ struct Config<2, 1> {
 #endif
 template <int WAVELET, int DIR, int SCHEME>
 struct SchemeConfig : Config<WAVELET, DIR> {};
+// Geometry of the direct-load instantiation of a program (see WL_DIRECT_R).
+template <int WAVELET, int DIR, int SCHEME, class C = SchemeConfig<WAVELET, DIR, SCHEME>>
+struct DirectConfigOf : C {  // forwards only (inverses keep the TMA geometry); WL_DIRECT_R=0 off
+    static constexpr bool kOwn = DIR == 0 && WL_DIRECT_R > 0;
+    static constexpr int R =
+        !kOwn ? C::R : (WL_DIRECT_R > 2 * C::KR ? WL_DIRECT_R : 2 * C::KR);
+    static constexpr int NW = !kOwn || C::NW < 8 ? C::NW : 8;  // 2 x 288 threads: <= 113 regs
+};
 #if WL_POLY_INV_CPT4
 #ifndef WL_POLY_R
 #define WL_POLY_R 3
