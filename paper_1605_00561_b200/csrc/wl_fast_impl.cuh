@@ -1399,8 +1399,11 @@ struct Config;
 #ifndef WL_MAXB97I
 #define WL_MAXB97I 2
 #endif
+// cdf53 forwards: 4 x 8 warps, 2-stage ring since the dynamic tile claims
+// (3 x 8 with 3 stages before; 8192^2 -2..-5%, configs[4] 0.89 -> 0.94 of the
+// copy peak, profiles/tuning_r02_s2.txt); Polyphase(*) keep 3 x 8 x 3 stages.
 #ifndef WL_NS53F
-#define WL_NS53F 3
+#define WL_NS53F 2
 #endif
 #ifndef WL_NS53I
 #define WL_NS53I 2
@@ -1412,7 +1415,7 @@ struct Config;
 #define WL_NS97I 2
 #endif
 #ifndef WL_R53F
-#define WL_R53F 3
+#define WL_R53F 4
 #endif
 #ifndef WL_NW53F
 #define WL_NW53F 8
@@ -1577,6 +1580,15 @@ template <>
 struct SchemeConfig<1, 0, 3> : Fwd97IE<3> {};
 template <>
 struct SchemeConfig<1, 0, 4> : Fwd97IE<4> {};
+
+template <int SCHEME>
+struct Fwd53Poly : Config<0, 0> {
+    static constexpr int R = 3, NS = 3;
+};
+template <>
+struct SchemeConfig<0, 0, 7> : Fwd53Poly<7> {};
+template <>
+struct SchemeConfig<0, 0, 8> : Fwd53Poly<8> {};
 
 // Tuning knob: one extra per-scheme override from the compiler command line
 // (-DWL_OVR_W=w -DWL_OVR_D=d -DWL_OVR_S=s -DWL_OVR_R=.. -DWL_OVR_NW=.. -DWL_OVR_NS=..
