@@ -1426,8 +1426,9 @@ struct Config;
 #ifndef WL_NW97F
 #define WL_NW97F 8
 #endif
+// cdf53 inverses: 4 x 8 (round 2, dynamic claims): 8192^2 -2..-8% over 3 x 8
 #ifndef WL_R53I
-#define WL_R53I 3
+#define WL_R53I 4
 #endif
 #ifndef WL_NW53I
 #define WL_NW53I 8
