@@ -226,6 +226,23 @@ def test_dd137_small(wl, oracle, engine):
         wl.set_engine(0)
 
 
+def test_dynamic_claim_slots_reused(wl):
+    """Dynamic tile claims (more tiles than resident CTAs): each launch takes a
+    counter slot of a 4096-slot ring that its last CTA resets; 4200 launches
+    wrap the ring and every result stays bit-identical (a slot left non-zero
+    would skip or repeat tiles)."""
+    import torch
+    img = torch.rand((2048, 2048), device="cuda")
+    sch = wl.build_scheme("monolithic", "cdf53")
+    q = wl.forward(img, sch)
+    want = wl.inverse(q, "cdf53", scheme="monolithic")
+    out = torch.empty_like(want)
+    for k in range(4200):
+        wl.inverse(q, "cdf53", scheme="monolithic", out=out)
+        if k % 700 == 0 or k == 4199:
+            assert torch.equal(out, want), k
+
+
 def test_errors(wl):
     import torch
     s = wl.build_scheme("sweldens", "cdf53")
