@@ -56,10 +56,18 @@ unsigned* sched_slot(cudaStream_t stream) {
     std::lock_guard<std::mutex> lk(mu);
     if (!ring[dev]) {
         if (cs != cudaStreamCaptureStatusNone) return nullptr;  // no allocation while capturing
+        // relaxed capture mode: a global-mode capture in another thread must
+        // not be invalidated by this one-time allocation; zeroed on the
+        // (non-capturing) caller stream and waited for there only
+        cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
+        cudaThreadExchangeStreamCaptureMode(&mode);
         unsigned* p = nullptr;
-        if (cudaMalloc(&p, sizeof(unsigned) * 2 * kSlots) != cudaSuccess ||
-            cudaMemset(p, 0, sizeof(unsigned) * 2 * kSlots) != cudaSuccess ||
-            cudaDeviceSynchronize() != cudaSuccess) {
+        const bool ok = cudaMalloc(&p, sizeof(unsigned) * 2 * kSlots) == cudaSuccess &&
+                        cudaMemsetAsync(p, 0, sizeof(unsigned) * 2 * kSlots, stream) == cudaSuccess &&
+                        cudaStreamSynchronize(stream) == cudaSuccess;
+        cudaThreadExchangeStreamCaptureMode(&mode);
+        if (!ok) {
+            if (p) cudaFree(p);
             cudaGetLastError();
             return nullptr;
         }
