@@ -1581,6 +1581,18 @@ template <>
 struct SchemeConfig<1, 0, 3> : Fwd97IE<3> {};
 template <>
 struct SchemeConfig<1, 0, 4> : Fwd97IE<4> {};
+// cdf97 Polyphase* forward (one 4x4 matrix epoch of reach 1 after the local
+// steps): A/B knobs, default = the generic cdf97 forward geometry.
+#ifndef WL_R97F_PS
+#define WL_R97F_PS WL_R97F
+#endif
+#ifndef WL_NW97F_PS
+#define WL_NW97F_PS WL_NW97F
+#endif
+template <>
+struct SchemeConfig<1, 0, 8> : Config<1, 0> {
+    static constexpr int R = WL_R97F_PS, NW = WL_NW97F_PS;
+};
 
 template <int SCHEME>
 struct Fwd53Poly : Config<0, 0> {
