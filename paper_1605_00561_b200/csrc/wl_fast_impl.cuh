@@ -148,6 +148,9 @@ __device__ __forceinline__ void mbar_wait_backoff(uint64_t* b, unsigned parity) 
 #ifndef WL_CLAIM_LATE
 #define WL_CLAIM_LATE 0
 #endif
+#ifndef WL_RAMP1
+#define WL_RAMP1 0
+#endif
 // A/B knobs: border tiles of periodic plans from the TMA box + wrapped
 // re-reads of the outside cells (1) or every cell from global memory (0);
 // periodic grid from cell 0 with clamped last row/column (1) or the former
@@ -640,6 +643,9 @@ __global__ void __launch_bounds__((NW + 1) * 32,
                     halo_ready = true;
                 }
                 float* dst = stage + s * G::kStageFloats;
+                // WL_RAMP1: the second tile's box only after the first one landed
+                // (the first tiles of all CTAs do not share HBM with the second ones)
+                if (WL_RAMP1 && i == 1) mbar_wait_backoff<64>(&full[0], 0);
                 mbar_expect_tx(&full[s], G::kStageBytes);
                 if (DIR == 0) {
                     constexpr int kSplitRows = 2 * G::kRows / WL_FWD_SPLIT;
@@ -692,6 +698,9 @@ __global__ void __launch_bounds__((NW + 1) * 32,
                 if (i >= NS) mbar_wait_backoff<ProdBackoff<P, DIR>::ns>(&empty[s], (use - 1) & 1);
 #endif
                 float* dst = stage + s * G::kStageFloats;
+                // WL_RAMP1: the second tile's box only after the first one landed
+                // (the first tiles of all CTAs do not share HBM with the second ones)
+                if (WL_RAMP1 && i == 1) mbar_wait_backoff<64>(&full[0], 0);
                 mbar_expect_tx(&full[s], G::kStageBytes);
                 if (DIR == 0) {
                     constexpr int kSplitRows = 2 * G::kRows / WL_FWD_SPLIT;
