@@ -1,7 +1,10 @@
 """Barrier structure on real SASS (the reference checks it on its simulator,
 acceptance.cpp:236-254 / test_parsim.cpp:101-115): every fast-engine kernel
-contains exactly count_barriers(scheme) block barriers -- the initial
-data-availability barrier plus one per epoch after the first -- and the
+contains exactly count_barriers(scheme) block barriers: per tile, the
+data-availability barrier is an mbarrier phase wait on the TMA stage
+(SYNCS.PHASECHK, counted separately) and every epoch after the first is one
+named bar.sync of the compute warps (count_barriers - 1 of them); the one
+CTA-wide bar.sync after the mbarrier initialisation completes the total. The
 compile-time negative control WL_BREAK_BARRIER drops exactly one (racecheck
 flags the resulting hazard: test_gpu_race.py). CPU-only: cuobjdump on the
 built library."""
@@ -33,10 +36,19 @@ def barrier_counts(lib_path):
             fn = km.groups() + (name,) if km else None
             if fn:
                 counts.setdefault(fn, 0)
+                kinds_of.setdefault(fn, {"init": 0, "epoch": 0, "wait": 0})
             continue
         if fn and re.search(r"\bBAR\.(SYNC|RED|ARV)", line):
             counts[fn] += 1
+            # bar.sync 0: the one CTA-wide barrier after the mbarrier init;
+            # bar.sync 1, NW*32: the per-tile epoch barriers of the compute warps
+            kinds_of[fn]["init" if re.search(r"BAR\.SYNC\S* 0x0 ;", line) else "epoch"] += 1
+        if fn and re.search(r"SYNCS\.PHASECHK", line):
+            kinds_of[fn]["wait"] += 1  # mbarrier waits (the per-tile data availability)
     return counts
+
+
+kinds_of = {}  # (wavelet, scheme, dir, name) -> {"init", "epoch", "wait"} (barrier_counts)
 
 
 @pytest.mark.skipif(not os.path.exists(CUOBJDUMP), reason="cuobjdump not available")
@@ -56,6 +68,12 @@ def test_sass_barriers_equal_count_barriers():
         kinds["direct"] += direct
         kinds["mirror"] += mirror
         assert n == want, (w, s, d, n, want)
+        # per tile: the data-availability wait (an mbarrier phase wait, not a
+        # bar.sync; the direct-load variant loads its own cells) + one named
+        # barrier per epoch after the first; plus the single init barrier
+        k = kinds_of[(w, s, d, name)]
+        assert k["init"] == 1 and k["epoch"] == want - 1, (w, s, d, k, want)
+        assert direct or k["wait"] >= 1, (w, s, d, k)
     assert kinds == {"direct": 36 + 14, "mirror": 36}, kinds
 
 
