@@ -36,6 +36,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <type_traits>
 #include <utility>
 
 #include "gen/fast_gen.cuh"
@@ -150,6 +151,14 @@ __device__ __forceinline__ void mbar_wait_backoff(uint64_t* b, unsigned parity) 
 #endif
 #ifndef WL_RAMP1
 #define WL_RAMP1 0
+#endif
+// Direct-load (unaligned) cdf53 forwards: realigned float4 stores (1) or
+// element-wise stores (0). Measured -8..-16% at 8190^2 for the cdf53 schemes
+// but Polyphase (+9%); the cdf97 direct kernels (96 registers) lose to the
+// extra spills; both keep the element-wise stores (profiles/tuning_r02_s2.txt,
+// tools/ab_runs/g6_realign.sh, g7_final.sh).
+#ifndef WL_REALIGN_STORES
+#define WL_REALIGN_STORES 1
 #endif
 // A/B knobs: border tiles of periodic plans from the TMA box + wrapped
 // re-reads of the outside cells (1) or every cell from global memory (0);
@@ -1238,7 +1247,54 @@ __global__ void __launch_bounds__((NW + 1) * 32,
 #pragma unroll
             for (int k = 0; k < (DIR == 0 ? 4 : 1); ++k) pk[k] = a.out[k] + b * a.out_bstride[k] + off0;
             const long step = DIR == 0 ? a.out_pitch : 2 * a.out_pitch;
-            if constexpr (DIRECT) {
+            if constexpr (DIRECT && DIR == 0 && CPT == 4 && WL_REALIGN_STORES && P::kHalo == 1 &&
+                          !std::is_same_v<P, P_cdf53_polyphase_fwd>) {
+                // Planes of any pitch / width: per plane row, the misalignment m
+                // of the lane's first cell is warp-uniform (lanes are 4 cells
+                // apart), so every lane stores the 16-byte block that starts
+                // (4 - m) & 3 cells into its own cells, completed by the next
+                // lane's first cells (shuffle) -- coalesced float4 rows; blocks
+                // that leave the stored columns fall back to masked scalars.
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const int qr = warp * R + r;
+                    const int gy = gy0 + r;
+                    if (!(qr >= H && qr < H + a.TH && gy >= a.ylo && gy < a.yhi)) continue;
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        float* const rp = pk[k] + r * step;
+                        const int m = static_cast<int>((reinterpret_cast<uintptr_t>(rp) >> 2) & 3);
+                        const int off = (4 - m) & 3;
+                        float w0, w1, w2, w3;
+                        if (m == 0) {
+                            w0 = v[r][0][k]; w1 = v[r][1][k]; w2 = v[r][2][k]; w3 = v[r][3][k];
+                        } else if (m == 1) {
+                            w0 = v[r][3][k];
+                            w1 = __shfl_down_sync(0xffffffffu, v[r][0][k], 1);
+                            w2 = __shfl_down_sync(0xffffffffu, v[r][1][k], 1);
+                            w3 = __shfl_down_sync(0xffffffffu, v[r][2][k], 1);
+                        } else if (m == 2) {
+                            w0 = v[r][2][k]; w1 = v[r][3][k];
+                            w2 = __shfl_down_sync(0xffffffffu, v[r][0][k], 1);
+                            w3 = __shfl_down_sync(0xffffffffu, v[r][1][k], 1);
+                        } else {
+                            w0 = v[r][1][k]; w1 = v[r][2][k]; w2 = v[r][3][k];
+                            w3 = __shfl_down_sync(0xffffffffu, v[r][0][k], 1);
+                        }
+                        const int cl = CPT * lane + off;  // first cell of the block
+                        const int gc = gx + off;          // its image cell column
+                        if (cl >= HX && cl + 3 < HX + a.TW && gc >= 0 && gc + 3 < a.qw) {
+                            *reinterpret_cast<float4*>(rp + off) = make_float4(w0, w1, w2, w3);
+                        } else {
+                            const float wv[4] = {w0, w1, w2, w3};
+#pragma unroll
+                            for (int t = 0; t < 4; ++t)
+                                if (cl + t >= HX && cl + t < HX + a.TW && gc + t >= 0 && gc + t < a.qw)
+                                    rp[off + t] = wv[t];
+                        }
+                    }
+                }
+            } else if constexpr (DIRECT) {
                 // element-wise stores under a per-cell column mask (any pitch,
                 // any plane width); row validity is warp-uniform
 #pragma unroll
