@@ -160,6 +160,12 @@ __device__ __forceinline__ void mbar_wait_backoff(uint64_t* b, unsigned parity) 
 #ifndef WL_REALIGN_STORES
 #define WL_REALIGN_STORES 1
 #endif
+// Direct-load inverses: float2 / float4 image-row stores (1) or element-wise (0).
+// Measured at 8190^2 / 8194^2: -4..-14% for every CPT = 2 inverse except the
+// cdf53 Polyphase(*) ones (+1..+7%, kept element-wise) (tools/ab_runs/g8_invpair.sh).
+#ifndef WL_INV_PAIR_STORES
+#define WL_INV_PAIR_STORES 1
+#endif
 // A/B knobs: border tiles of periodic plans from the TMA box + wrapped
 // re-reads of the outside cells (1) or every cell from global memory (0);
 // periodic grid from cell 0 with clamped last row/column (1) or the former
@@ -1291,6 +1297,41 @@ __global__ void __launch_bounds__((NW + 1) * 32,
                             for (int t = 0; t < 4; ++t)
                                 if (cl + t >= HX && cl + t < HX + a.TW && gc + t >= 0 && gc + t < a.qw)
                                     rp[off + t] = wv[t];
+                        }
+                    }
+                }
+            } else if constexpr (DIRECT && DIR == 1 && CPT == 2 && WL_INV_PAIR_STORES &&
+                                 !std::is_same_v<P, P_cdf53_polyphase_inv> &&
+                                 !std::is_same_v<P, P_cdf53_polyphase_star_inv>) {
+                // Inverse image rows of any width: the lane's two cells are 4
+                // consecutive pixels per row. Even pitch and base: float2 pairs,
+                // or one float4 where the row's address is 16-byte aligned
+                // (warp-uniform per row: lanes are 4 pixels apart); otherwise
+                // element-wise. Per-cell column masks as below.
+                const bool al8 = ((reinterpret_cast<uintptr_t>(a.out[0]) & 7) == 0) &&
+                                 (a.out_pitch & 1) == 0 && (a.out_bstride[0] & 1) == 0;
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const int qr = warp * R + r;
+                    const int gy = gy0 + r;
+                    if (!(qr >= H && qr < H + a.TH && gy >= a.ylo && gy < a.yhi)) continue;
+                    const int cl = CPT * lane;
+                    const bool ok0 = cl >= HX && cl < HX + a.TW && gx >= 0 && gx < a.qw;
+                    const bool ok1 = cl + 1 >= HX && cl + 1 < HX + a.TW && gx + 1 >= 0 && gx + 1 < a.qw;
+                    float* const p0 = pk[0] + r * step;
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {  // pixel rows 2y (LL HL) and 2y+1 (LH HH)
+                        float* const p = p0 + h * a.out_pitch;
+                        const float x0 = v[r][0][2 * h], x1 = v[r][0][2 * h + 1];
+                        const float x2 = v[r][1][2 * h], x3 = v[r][1][2 * h + 1];
+                        if (al8 && ok0 && ok1 && (reinterpret_cast<uintptr_t>(p) & 15) == 0) {
+                            *reinterpret_cast<float4*>(p) = make_float4(x0, x1, x2, x3);
+                        } else if (al8) {
+                            if (ok0) *reinterpret_cast<float2*>(p) = make_float2(x0, x1);
+                            if (ok1) *reinterpret_cast<float2*>(p + 2) = make_float2(x2, x3);
+                        } else {
+                            if (ok0) { p[0] = x0; p[1] = x1; }
+                            if (ok1) { p[2] = x2; p[3] = x3; }
                         }
                     }
                 }
