@@ -152,13 +152,16 @@ __device__ __forceinline__ void mbar_wait_backoff(uint64_t* b, unsigned parity) 
 #ifndef WL_RAMP1
 #define WL_RAMP1 0
 #endif
-// Direct-load (unaligned) cdf53 forwards: realigned float4 stores (1) or
-// element-wise stores (0). Measured -8..-16% at 8190^2 for the cdf53 schemes
-// but Polyphase (+9%); the cdf97 direct kernels (96 registers) lose to the
-// extra spills; both keep the element-wise stores (profiles/tuning_r02_s2.txt,
-// tools/ab_runs/g6_realign.sh, g7_final.sh).
+// Direct-load (unaligned) forwards: realigned float4 stores (1) or
+// element-wise stores (0); WL_REALIGN97 extends them to cdf97. With 3-row warps
+// (WL_DIRECT_R = 3) every lifting forward gains (8190^2: cdf53 -8..-16%, cdf97
+// -6..-16%) except the Polyphase ones, which keep element-wise stores (and
+// 4-row warps for cdf97) (profiles/tuning_r02_s2.txt, tools/ab_runs/g6, g7, g10).
 #ifndef WL_REALIGN_STORES
 #define WL_REALIGN_STORES 1
+#endif
+#ifndef WL_REALIGN97
+#define WL_REALIGN97 1
 #endif
 // Direct-load inverses: float2 / float4 image-row stores (1) or element-wise (0).
 // Measured at 8190^2 / 8194^2: -4..-14% for every CPT = 2 inverse except the
@@ -533,7 +536,7 @@ constexpr int xch_comps() {
 // (WL_DIRECT_R, at least 2 x reach; DirectConfig) and WL_DIRECT_MINB CTAs per
 // SM let a second CTA's loads overlap the first one's compute.
 #ifndef WL_DIRECT_R
-#define WL_DIRECT_R 4
+#define WL_DIRECT_R 3  // 4 before the realigned stores (tools/ab_runs/g10_direct97.sh)
 #endif
 #ifndef WL_DIRECT_MINB
 #define WL_DIRECT_MINB 2
@@ -1253,8 +1256,10 @@ __global__ void __launch_bounds__((NW + 1) * 32,
 #pragma unroll
             for (int k = 0; k < (DIR == 0 ? 4 : 1); ++k) pk[k] = a.out[k] + b * a.out_bstride[k] + off0;
             const long step = DIR == 0 ? a.out_pitch : 2 * a.out_pitch;
-            if constexpr (DIRECT && DIR == 0 && CPT == 4 && WL_REALIGN_STORES && P::kHalo == 1 &&
-                          !std::is_same_v<P, P_cdf53_polyphase_fwd>) {
+            if constexpr (DIRECT && DIR == 0 && CPT == 4 && WL_REALIGN_STORES &&
+                          (P::kHalo == 1 || WL_REALIGN97) &&
+                          !std::is_same_v<P, P_cdf53_polyphase_fwd> &&
+                          !std::is_same_v<P, P_cdf97_polyphase_fwd>) {
                 // Planes of any pitch / width: per plane row, the misalignment m
                 // of the lane's first cell is warp-uniform (lanes are 4 cells
                 // apart), so every lane stores the 16-byte block that starts
@@ -1629,8 +1634,9 @@ struct SchemeConfig : Config<WAVELET, DIR> {};
 template <int WAVELET, int DIR, int SCHEME, class C = SchemeConfig<WAVELET, DIR, SCHEME>>
 struct DirectConfigOf : C {  // forwards only (inverses keep the TMA geometry); WL_DIRECT_R=0 off
     static constexpr bool kOwn = DIR == 0 && WL_DIRECT_R > 0;
-    static constexpr int R =
-        !kOwn ? C::R : (WL_DIRECT_R > 2 * C::KR ? WL_DIRECT_R : 2 * C::KR);
+    // cdf97 Polyphase forward: 4-row warps (its 126-MAC epoch is 14% slower on 3)
+    static constexpr int kR = WAVELET == 1 && SCHEME == 7 && WL_DIRECT_R == 3 ? 4 : WL_DIRECT_R;
+    static constexpr int R = !kOwn ? C::R : (kR > 2 * C::KR ? kR : 2 * C::KR);
     static constexpr int NW = !kOwn || C::NW < 8 ? C::NW : 8;  // 2 x 288 threads: <= 113 regs
 };
 #if WL_POLY_INV_CPT4
