@@ -165,7 +165,8 @@ __device__ __forceinline__ void mbar_wait_backoff(uint64_t* b, unsigned parity) 
 #endif
 // Direct-load inverses: float2 / float4 image-row stores (1) or element-wise (0).
 // Measured at 8190^2 / 8194^2: -4..-14% for every CPT = 2 inverse except the
-// cdf53 Polyphase(*) ones (+1..+7%, kept element-wise) (tools/ab_runs/g8_invpair.sh).
+// cdf53 Polyphase(*) ones (+1..+7%, kept element-wise) (tools/ab_runs/g8_invpair.sh);
+// the CPT = 4 cdf97 Polyphase inverse 0.373 -> 0.234 ms (g13_inv4.sh).
 #ifndef WL_INV_PAIR_STORES
 #define WL_INV_PAIR_STORES 1
 #endif
@@ -1337,6 +1338,55 @@ __global__ void __launch_bounds__((NW + 1) * 32,
                         } else {
                             if (ok0) { p[0] = x0; p[1] = x1; }
                             if (ok1) { p[2] = x2; p[3] = x3; }
+                        }
+                    }
+                }
+            } else if constexpr (DIRECT && DIR == 1 && CPT == 4 && WL_INV_PAIR_STORES) {
+                // Same for the CPT = 4 inverses (cdf97 Polyphase): 8 consecutive
+                // pixels per lane and row -- two float4, or float2 + float4 +
+                // float2 when the row is 8- but not 16-byte aligned.
+                const bool al8 = ((reinterpret_cast<uintptr_t>(a.out[0]) & 7) == 0) &&
+                                 (a.out_pitch & 1) == 0 && (a.out_bstride[0] & 1) == 0;
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const int qr = warp * R + r;
+                    const int gy = gy0 + r;
+                    if (!(qr >= H && qr < H + a.TH && gy >= a.ylo && gy < a.yhi)) continue;
+                    bool okc[4];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const int cl = CPT * lane + j;
+                        okc[j] = cl >= HX && cl < HX + a.TW && gx + j >= 0 && gx + j < a.qw;
+                    }
+                    const bool all = okc[0] && okc[1] && okc[2] && okc[3];
+                    float* const p0 = pk[0] + r * step;
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {  // pixel rows 2y (LL HL) and 2y+1 (LH HH)
+                        float* const p = p0 + h * a.out_pitch;
+                        float x[8];
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            x[2 * j] = v[r][j][2 * h];
+                            x[2 * j + 1] = v[r][j][2 * h + 1];
+                        }
+                        if (al8 && all && (reinterpret_cast<uintptr_t>(p) & 15) == 0) {
+                            *reinterpret_cast<float4*>(p) = make_float4(x[0], x[1], x[2], x[3]);
+                            *reinterpret_cast<float4*>(p + 4) = make_float4(x[4], x[5], x[6], x[7]);
+                        } else if (al8 && all) {
+                            *reinterpret_cast<float2*>(p) = make_float2(x[0], x[1]);
+                            *reinterpret_cast<float4*>(p + 2) = make_float4(x[2], x[3], x[4], x[5]);
+                            *reinterpret_cast<float2*>(p + 6) = make_float2(x[6], x[7]);
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < 4; ++j) {
+                                if (!okc[j]) continue;
+                                if (al8) {
+                                    *reinterpret_cast<float2*>(p + 2 * j) = make_float2(x[2 * j], x[2 * j + 1]);
+                                } else {
+                                    p[2 * j] = x[2 * j];
+                                    p[2 * j + 1] = x[2 * j + 1];
+                                }
+                            }
                         }
                     }
                 }
