@@ -536,6 +536,9 @@ constexpr int xch_comps() {
 // exchange), so its occupancy is set by registers: shorter warp rows
 // (WL_DIRECT_R, at least 2 x reach; DirectConfig) and WL_DIRECT_MINB CTAs per
 // SM let a second CTA's loads overlap the first one's compute.
+#ifndef WL_DIRECT_NW
+#define WL_DIRECT_NW 8
+#endif
 #ifndef WL_DIRECT_R
 #define WL_DIRECT_R 3  // 4 before the realigned stores (tools/ab_runs/g10_direct97.sh)
 #endif
@@ -1687,7 +1690,7 @@ struct DirectConfigOf : C {  // forwards only (inverses keep the TMA geometry); 
     // cdf97 Polyphase forward: 4-row warps (its 126-MAC epoch is 14% slower on 3)
     static constexpr int kR = WAVELET == 1 && SCHEME == 7 && WL_DIRECT_R == 3 ? 4 : WL_DIRECT_R;
     static constexpr int R = !kOwn ? C::R : (kR > 2 * C::KR ? kR : 2 * C::KR);
-    static constexpr int NW = !kOwn || C::NW < 8 ? C::NW : 8;  // 2 x 288 threads: <= 113 regs
+    static constexpr int NW = !kOwn || C::NW < WL_DIRECT_NW ? C::NW : WL_DIRECT_NW;  // 2 x 288 threads: <= 113 regs
 };
 #if WL_POLY_INV_CPT4
 #ifndef WL_POLY_R
