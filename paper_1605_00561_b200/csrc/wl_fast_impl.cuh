@@ -156,7 +156,8 @@ __device__ __forceinline__ void mbar_wait_backoff(uint64_t* b, unsigned parity) 
 // element-wise stores (0); WL_REALIGN97 extends them to cdf97. With 3-row warps
 // (WL_DIRECT_R = 3) every lifting forward gains (8190^2: cdf53 -8..-16%, cdf97
 // -6..-16%) except the Polyphase ones, which keep element-wise stores (and
-// 4-row warps for cdf97) (profiles/tuning_r02_s2.txt, tools/ab_runs/g6, g7, g10).
+// 4-row warps for cdf97), and the reach-2 dd137 kernels (+8..10%)
+// (profiles/tuning_r02_s2.txt, tools/ab_runs/g6, g7, g10, g16).
 #ifndef WL_REALIGN_STORES
 #define WL_REALIGN_STORES 1
 #endif
@@ -1261,7 +1262,7 @@ __global__ void __launch_bounds__((NW + 1) * 32,
             for (int k = 0; k < (DIR == 0 ? 4 : 1); ++k) pk[k] = a.out[k] + b * a.out_bstride[k] + off0;
             const long step = DIR == 0 ? a.out_pitch : 2 * a.out_pitch;
             if constexpr (DIRECT && DIR == 0 && CPT == 4 && WL_REALIGN_STORES &&
-                          (P::kHalo == 1 || WL_REALIGN97) &&
+                          (P::kHalo == 1 || (WL_REALIGN97 && P::kReach == 1)) &&
                           !std::is_same_v<P, P_cdf53_polyphase_fwd> &&
                           !std::is_same_v<P, P_cdf97_polyphase_fwd>) {
                 // Planes of any pitch / width: per plane row, the misalignment m

@@ -292,6 +292,24 @@ def test_unaligned_shapes_vs_oracle(wl, oracle, wavelet):
                       ("inv", s, b, h, w))
 
 
+def test_unaligned_shapes_dd137_vs_oracle(wl, oracle):
+    """dd137 (reach 2) lifting schemes on unaligned shapes: the direct-load
+    variant (realigned float4 plane stores, vector image-row stores) vs the
+    oracle, periodic and symmetric, forward and inverse."""
+    for (h, w) in [(1030, 1022), (516, 1028), (262, 1030)]:
+        img = uniform_f32(h, w, h + w)
+        dev = gpu(img)
+        for s in SCHEMES[:7]:
+            sch = wl.build_scheme(s, "dd137")
+            for b in BOUNDARIES:
+                want = oracle.forward(img, "dd137", s, b)
+                q = wl.forward(dev, sch, b)
+                check(host(q), want, False, (s, b, h, w))
+                want_rec = oracle.inverse(host(q), "dd137", b, scheme=s)
+                check(host(wl.inverse(q, "dd137", b, scheme=s)), want_rec, False,
+                      ("inv", s, b, h, w))
+
+
 @pytest.mark.parametrize("wavelet", ["cdf53", "cdf97", "dd137"])
 def test_direct_path_equals_tma_path(wl, wavelet):
     """The direct-load variant (engine 3, forced) runs the same instruction
